@@ -1,0 +1,161 @@
+/*
+ * somb200 -- C ABI of the B200-native batch-SOM epoch hot path.
+ *
+ * Every entry point takes DEVICE pointers, enqueues its work on `stream`
+ * (a cudaStream_t passed as void*), never allocates, never synchronises the
+ * host, and returns SOMB_OK or a SOMB_E_* status (message: somb_last_error()).
+ * Status -> reference exception family (errors.py): SOMB_E_CONFIG ->
+ * InvalidConfig (exit 1), SOMB_E_INPUT -> InputError/DimensionMismatch
+ * (exit 2), SOMB_E_CUDA / SOMB_E_ARCH -> SomkitError (exit 3).
+ *
+ * The reference (somkit, pure Python + numpy/OpenBLAS) has no FFI of its
+ * own; each function below cites the reference routine it replaces
+ * (paths relative to /root/reference/pkg/src/somkit/).  INTEGRATION.md shows
+ * the ctypes binding a somkit maintainer would add.
+ *
+ * Layouts (HBM): X f32 [n][d] row-major; CSR (int64 offsets, int32 sorted
+ * cols, f32 vals); codebook W f32 [K][d], K = n_columns*n_rows, flat
+ * row-major node order (kernels.py:89-96); fp16 screening copies use a row
+ * pitch dp = round_up(d, 8) and K padded to kp = round_up(K, 256).
+ */
+#ifndef SOMB200_H
+#define SOMB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SOMB_API __attribute__((visibility("default")))
+#else
+#define SOMB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SOMB_OK 0
+#define SOMB_E_CONFIG 1
+#define SOMB_E_INPUT 2
+#define SOMB_E_CUDA 3
+#define SOMB_E_ARCH 4
+
+#define SOMB_GRID_RECT 0      /* grid.py lattice (reference)            */
+#define SOMB_GRID_HEX 1       /* extension: offset-row hexagonal         */
+#define SOMB_PLANAR 0         /* grid.py:15-17                           */
+#define SOMB_TOROID 1
+#define SOMB_NBH_GAUSSIAN 0   /* exp(-d/r), train.py:138-144             */
+#define SOMB_NBH_BUBBLE 1     /* extension: 1 if d <= r                  */
+#define SOMB_DIST_BLOCKED 1   /* d2 = -2x.w + |x|^2 + |w|^2 (kernels.py:195-205) */
+#define SOMB_DIST_NAIVE 0     /* d2 = sum (w - x)^2       (kernels.py:182-192) */
+
+typedef struct somb_map {
+    int32_t n_columns, n_rows;  /* x extent, y extent                    */
+    int32_t grid;               /* SOMB_GRID_*                           */
+    int32_t topology;           /* SOMB_PLANAR / SOMB_TOROID             */
+} somb_map;
+
+typedef struct somb_hood {
+    int32_t neighborhood;       /* SOMB_NBH_*                            */
+    int32_t compact;            /* 1: h = 0 beyond radius (extension)    */
+    double radius;              /* epoch radius (train.py:209-217)       */
+    double cutoff;              /* h < cutoff -> 0 (kernels.py:146-147)  */
+} somb_hood;
+
+/* Screening parameters of the tensor-core BMU search. */
+#define SOMB_CAND_CAP 32        /* candidates kept per row               */
+
+SOMB_API const char *somb_version(void);
+SOMB_API const char *somb_last_error(void);
+/* 0 if device `dev` is sm_100 (B200) and the library's kernels load. */
+SOMB_API int somb_device_check(int dev);
+
+/* ---- dense dataset, once per dataset ---------------------------------
+ * nu = per-feature mean of X (fp64 fixed-order sum, rounded to f32), the
+ * data-side centring of the screen.  Replaces: nothing (the reference
+ * screens in fp64 directly); enables kernels.py:195-205 on fp16 tensor
+ * cores.  ws: >= somb_data_stats_ws(d) bytes. */
+SOMB_API size_t somb_data_stats_ws(int32_t d);
+SOMB_API int somb_data_stats(const float *X, int64_t n, int32_t d, float *nu,
+                    float *absmax /* [1] max|x - nu| */, void *ws, void *stream);
+/* Xh[i][k] = fp16((x_ik - nu_k) * 2^xexp) (pitch dp, zero pad); xnorm[i] =
+ * |x_i - nu|_2 (f32); x2[i] = |x_i|^2 in fp64 (kernels.py:198). */
+SOMB_API int somb_data_pack(const float *X, int64_t n, int32_t d, const float *nu,
+                   int32_t xexp, uint16_t *Xh, int32_t dp, float *xnorm,
+                   double *x2, void *stream);
+
+/* ---- codebook, once per epoch ----------------------------------------
+ * mu = mean_j W_j; delta_j = W_j - mu (exact in fp64); Wh = fp16(delta *
+ * 2^s) with s picked on device from max|delta|; c_j = |delta_j|^2 +
+ * 2 (mu - nu).delta_j (f32, +inf on padding and duplicate rows);
+ * w2_j = |w_j|^2 fp64 (kernels.py:389-390); scal[0..3] = {m, nmax, ...}
+ * device scalars consumed by somb_bmu_dense.  ws >= somb_codebook_ws(K, d). */
+SOMB_API size_t somb_codebook_ws(int32_t K, int32_t d);
+SOMB_API int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const float *nu,
+                          int32_t xexp, uint16_t *Wh, int32_t dp, int32_t kp,
+                          float *c, double *w2, float *scal, void *ws,
+                          void *stream);
+
+/* ---- BMU search (kernels.py:195-205 / 182-192, :407) -----------------
+ * fp16 tensor-core screen (tcgen05, TMEM accumulators, TMA-staged tiles)
+ * keeping per row every node within the screening window (<= CAP, the
+ * lowest screened values when truncated), then an exact fp64 re-rank of
+ * the candidates with the reference formula `dist_mode`, first-minimum
+ * ties.  Output bmu int32[n], d2min fp64[n] (clamped >= 0), flags int32[n]
+ * (bit0 = window truncated).  ws >= somb_bmu_ws(n).  screen_impl: 0 =
+ * tcgen05 (sm_100a), 1 = SIMT reference screen (tests). */
+SOMB_API size_t somb_bmu_ws(int64_t n);
+SOMB_API int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xnorm,
+                   const double *x2, int64_t n, int32_t d, int32_t dp,
+                   const uint16_t *Wh, const float *W, const float *c,
+                   const double *w2, int32_t K, int32_t kp, const float *scal,
+                   float window_coef, int32_t dist_mode, int32_t screen_impl,
+                   int32_t *bmu, double *d2min, int32_t *flags, void *ws,
+                   void *stream);
+
+/* qe_sum = sum_i sqrt(d2min_i) in fixed order (kernels.py:407, 427). */
+SOMB_API int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws,
+                void *stream);
+
+/* ---- batch update: node sums (BMU histogram + per-node data sums) ----
+ * S_b = sum_{i: bmu_i = b} x_i in ascending i (fp64), cnt_b = |{i}|;
+ * a stable device radix sort groups the rows.  Together with
+ * somb_hood_update this replaces the accumulate of kernels.py:225-226
+ * (num = H S, den = H cnt).  ws >= somb_node_sums_ws(n, K). */
+SOMB_API size_t somb_node_sums_ws(int64_t n, int32_t d, int32_t K);
+SOMB_API int somb_node_sums_dense(const float *X, int64_t n, int32_t d,
+                         const int32_t *bmu, int32_t K, double *S, double *cnt,
+                         void *ws, void *stream);
+
+/* ---- batch update: neighbourhood convolution + blend ------------------
+ * h(b, j) from grid offsets (kernels.py:99-150; hex/bubble/compact are
+ * extensions), den_j = sum_b h cnt_b, num_j = sum_b h S_b (fp64), then for
+ * nodes [node_begin, node_end): W_new_j = f32((1-scale) W_j + scale num_j /
+ * den_j) if den_j > 0 else W_j bit-exact (kernels.py:438-450).
+ * num_out / den_out (K x d / K, may be NULL) expose the accumulators for the
+ * reference-compatible search_accumulate debug path.
+ * dist_table (may be NULL): grid distance per wrapped offset [dy][dx]
+ * (rect: n_rows x n_columns) -- the host passes numpy's hypot table so d is
+ * bit-identical to kernels.py:112; NULL computes sqrt(dx^2 + dy^2).
+ * ws >= somb_hood_ws(map, K). */
+SOMB_API size_t somb_hood_ws(const somb_map *map, int32_t K);
+SOMB_API int somb_hood_update(const double *S, const double *cnt, int32_t d,
+                     const somb_map *map, const somb_hood *hood, double scale,
+                     const double *dist_table,
+                     const float *W_old, int32_t node_begin, int32_t node_end,
+                     float *W_new, double *num_out, double *den_out, void *ws,
+                     void *stream);
+
+/* Standalone blend of given accumulators (kernels.py:438-450), same
+ * arithmetic as the fused epilogue of somb_hood_update. */
+SOMB_API int somb_blend(const float *W_old, const double *num, const double *den,
+               int32_t K, int32_t d, double scale, float *W_new, void *stream);
+
+/* ---- U-matrix (umatrix.py:26-45; hex adjacency = extension) ---------- */
+SOMB_API int somb_umatrix(const float *W, int32_t d, const somb_map *map, float *U,
+                 void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOMB200_H */

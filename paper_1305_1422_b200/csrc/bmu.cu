@@ -1,0 +1,217 @@
+// BMU search: screen (tensor-core or SIMT) -> candidates -> exact fp64 re-rank.
+//
+// Replaces kernels.py:195-205 (_search_chunk_blocked), :182-192 (naive) and
+// the qe sum of :407.  The screen ranks r_ij = c_j - 2 x'_i.delta_j on fp16
+// operands (prep.cu); the re-rank evaluates the reference formula in fp64
+// from the original f32 rows, so the returned BMU is the reference's argmin
+// whenever it lies in the screened candidate set.
+#include "cand.cuh"
+
+namespace somb {
+
+int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int kp,
+                     const float *c, const float *xnorm, const float *scal, float wcoef,
+                     int *cand, int *ccount, int *flags, cudaStream_t st);
+
+// --------------------------------------------------------- SIMT screen (v0)
+// Reference implementation of the screen used by the parity tests to check
+// the tcgen05 kernel (same fp16 operands, fp32 FMA accumulation).
+constexpr int kSimtRows = 128;
+constexpr int kSimtCols = 32;
+constexpr int kSimtK = 64;
+
+__global__ void __launch_bounds__(kSimtRows)
+screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __half *__restrict__ Wh,
+                   int kp, const float *__restrict__ c, const float *__restrict__ xnorm,
+                   const float *__restrict__ scal, float wcoef, int *__restrict__ cand,
+                   int *__restrict__ ccount, int *__restrict__ flags) {
+    __shared__ float wt[kSimtCols][kSimtK + 1];
+    __shared__ float bv[SOMB_CAND_CAP * kSimtRows];
+    __shared__ int bi[SOMB_CAND_CAP * kSimtRows];
+    const int t = threadIdx.x;
+    const int64_t row = (int64_t)blockIdx.x * kSimtRows + t;
+    const bool live = row < n;
+    const float m = scal[0];
+    const float nmax = scal[1];
+    CandRow<SOMB_CAND_CAP> st;
+    cand_init(st, live ? wcoef * xnorm[row] * nmax : 0.0f);
+    const __half *xr = Xh + (live ? row : 0) * (int64_t)dp;
+    for (int j0 = 0; j0 < kp; j0 += kSimtCols) {
+        float acc[kSimtCols];
+#pragma unroll
+        for (int q = 0; q < kSimtCols; ++q) acc[q] = 0.0f;
+        for (int k0 = 0; k0 < dp; k0 += kSimtK) {
+            __syncthreads();
+            for (int e = t; e < kSimtCols * kSimtK; e += kSimtRows) {
+                int jj = e / kSimtK, kk = e % kSimtK;
+                int k = k0 + kk;
+                wt[jj][kk] = k < dp ? __half2float(Wh[(int64_t)(j0 + jj) * dp + k]) : 0.0f;
+            }
+            __syncthreads();
+            float xv[kSimtK];
+#pragma unroll
+            for (int kk = 0; kk < kSimtK; ++kk) {
+                int k = k0 + kk;
+                xv[kk] = (live && k < dp) ? __half2float(xr[k]) : 0.0f;
+            }
+#pragma unroll 4
+            for (int q = 0; q < kSimtCols; ++q) {
+                float a = acc[q];
+#pragma unroll
+                for (int kk = 0; kk < kSimtK; ++kk) a = fmaf(xv[kk], wt[q][kk], a);
+                acc[q] = a;
+            }
+        }
+        if (live) {
+#pragma unroll 1
+            for (int q = 0; q < kSimtCols; ++q) {
+                float r = fmaf(acc[q], m, c[j0 + q]);
+                cand_push<SOMB_CAND_CAP>(st, r, j0 + q, bv + t, bi + t, kSimtRows);
+            }
+        }
+    }
+    if (live) {
+        int *out = cand + row * SOMB_CAND_CAP;
+        ccount[row] = cand_emit<SOMB_CAND_CAP>(st, bv + t, bi + t, kSimtRows, out);
+        flags[row] = st.trunc;
+    }
+}
+
+// ----------------------------------------------------------- fp64 re-rank
+// One warp per row; `all` = exact scan of every node (screen_impl 2 and the
+// empty-candidate safety net).
+__global__ void rerank_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n,
+                              int d, const float *__restrict__ W, const double *__restrict__ w2,
+                              int K, const int *__restrict__ cand, const int *__restrict__ ccount,
+                              int dist_mode, int all, int *__restrict__ bmu,
+                              double *__restrict__ d2min) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const float *x = X + row * d;
+    int cnt = all ? K : ccount[row];
+    bool scan_all = all || cnt <= 0;
+    if (scan_all) cnt = K;
+    double best = INFINITY;
+    int bestj = 0;
+    const double xx = x2[row];
+    for (int q = 0; q < cnt; ++q) {
+        int j = scan_all ? q : cand[row * SOMB_CAND_CAP + q];
+        const float *w = W + (int64_t)j * d;
+        double d2;
+        if (dist_mode == SOMB_DIST_NAIVE) {
+            double s = 0.0;
+            for (int k = lane; k < d; k += 32) {
+                double df = (double)w[k] - (double)x[k];
+                s = __fma_rn(df, df, s);
+            }
+            d2 = warp_sum(s);
+        } else {
+            double s = 0.0;
+            for (int k = lane; k < d; k += 32) s = __fma_rn((double)x[k], (double)w[k], s);
+            s = warp_sum(s);
+            // ((-2 dot) + |x|^2) + |w|^2, clamp >= 0 (kernels.py:196-202)
+            d2 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, s), xx), w2[j]);
+            d2 = fmax(d2, 0.0);
+        }
+        if (d2 < best) {   // ascending j: strict < keeps the first minimum
+            best = d2;
+            bestj = j;
+        }
+    }
+    if (lane == 0) {
+        bmu[row] = bestj;
+        d2min[row] = best;
+    }
+}
+
+// --------------------------------------------------------- qe reduction
+constexpr int kQeTile = 4096;
+
+__global__ void qe_partial(const double *__restrict__ d2min, int64_t n, double *__restrict__ part) {
+    __shared__ double sh[256];
+    int64_t base = (int64_t)blockIdx.x * kQeTile;
+    double s = 0.0;
+    for (int q = 0; q < kQeTile / 256; ++q) {
+        int64_t i = base + q * 256 + threadIdx.x;
+        if (i < n) s += sqrt(d2min[i]);
+    }
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void qe_final(const double *__restrict__ part, int np, double *__restrict__ out) {
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < np; i += 256) s += part[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+}  // namespace somb
+
+using namespace somb;
+
+extern "C" size_t somb_bmu_ws(int64_t n) {
+    return align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256) + align_up((size_t)n * sizeof(int), 256);
+}
+
+extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xnorm, const double *x2,
+                              int64_t n, int32_t d, int32_t dp, const uint16_t *Wh, const float *W,
+                              const float *c, const double *w2, int32_t K, int32_t kp,
+                              const float *scal, float window_coef, int32_t dist_mode,
+                              int32_t screen_impl, int32_t *bmu, double *d2min, int32_t *flags,
+                              void *ws, void *stream) {
+    SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && dp % 8 == 0 && kp >= K && kp % 256 == 0, SOMB_E_INPUT,
+                 "bmu_dense: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
+    SOMB_REQUIRE(dist_mode == SOMB_DIST_BLOCKED || dist_mode == SOMB_DIST_NAIVE, SOMB_E_CONFIG,
+                 "bmu_dense: bad dist_mode %d", dist_mode);
+    if (n == 0) return SOMB_OK;
+    cudaStream_t st = as_stream(stream);
+    int *cand = (int *)ws;
+    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
+    int all = 0;
+    if (screen_impl == 0) {
+        int rc = launch_screen_tc((const __half *)Xh, n, dp, (const __half *)Wh, kp, c, xnorm, scal,
+                                  window_coef, cand, ccount, flags, st);
+        if (rc != SOMB_OK) return rc;
+    } else if (screen_impl == 1) {
+        unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
+        screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh,
+                                                          kp, c, xnorm, scal, window_coef, cand, ccount,
+                                                          flags);
+        SOMB_LAUNCH_CHECK("screen_simt");
+    } else {
+        all = 1;
+        cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
+    }
+    const int wpb = 8;
+    rerank_kernel<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
+        X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, bmu, d2min);
+    SOMB_LAUNCH_CHECK("rerank");
+    return SOMB_OK;
+}
+
+extern "C" int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    int np = (int)((n + kQeTile - 1) / kQeTile);
+    if (np == 0) {
+        cudaMemsetAsync(out, 0, sizeof(double), st);
+        return SOMB_OK;
+    }
+    double *part = (double *)ws;   // >= np doubles (callers pass somb_bmu_ws-sized ws)
+    qe_partial<<<np, 256, 0, st>>>(d2min, n, part);
+    qe_final<<<1, 256, 0, st>>>(part, np, out);
+    SOMB_LAUNCH_CHECK("qe_sum");
+    return SOMB_OK;
+}

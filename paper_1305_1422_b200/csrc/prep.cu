@@ -1,0 +1,232 @@
+// Dataset and codebook preparation for the fp16 tensor-core screen.
+//
+// Screening identity: with nu = data mean, mu = codebook
+// mean, delta_j = w_j - mu, x'_i = x_i - nu,
+//   |x_i - w_j|^2 = |x_i - mu|^2 + r_ij,   r_ij = c_j - 2 x'_i . delta_j,
+//   c_j = |delta_j|^2 + 2 (mu - nu) . delta_j.
+// The row term |x_i - mu|^2 does not affect the argmin, so the screen ranks
+// r_ij; both operands are centred, which keeps the fp16 rounding error small
+// relative to the gaps between nodes after the codebook collapses
+// (SURVEY.md 7.3-1).
+#include "common.cuh"
+
+namespace somb {
+
+// ---------------------------------------------------------------- data stats
+// Stage 1: per (row-chunk, column) fp64 partial sum plus column min/max.
+constexpr int kStatChunks = 256;
+
+__global__ void data_stats_partial(const float *__restrict__ X, int64_t n, int d,
+                                   double *__restrict__ psum, float *__restrict__ pmin,
+                                   float *__restrict__ pmax) {
+    int col = blockIdx.x * blockDim.x + threadIdx.x;
+    int chunk = blockIdx.y;
+    if (col >= d) return;
+    int64_t per = (n + kStatChunks - 1) / kStatChunks;
+    int64_t a = chunk * per, b = min(n, a + per);
+    double s = 0.0;
+    float lo = INFINITY, hi = -INFINITY;
+    for (int64_t i = a; i < b; ++i) {
+        float v = X[i * d + col];
+        s += (double)v;
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+    }
+    psum[(int64_t)chunk * d + col] = s;
+    pmin[(int64_t)chunk * d + col] = lo;
+    pmax[(int64_t)chunk * d + col] = hi;
+}
+
+// Stage 2: fixed-order fold over chunks -> nu (f32) and max|x - nu|.
+__global__ void data_stats_final(const double *__restrict__ psum, const float *__restrict__ pmin,
+                                 const float *__restrict__ pmax, int64_t n, int d,
+                                 float *__restrict__ nu, float *__restrict__ absmax) {
+    int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= d) return;
+    double s = 0.0;
+    float lo = INFINITY, hi = -INFINITY;
+    for (int c = 0; c < kStatChunks; ++c) {
+        s += psum[(int64_t)c * d + col];
+        lo = fminf(lo, pmin[(int64_t)c * d + col]);
+        hi = fmaxf(hi, pmax[(int64_t)c * d + col]);
+    }
+    float m = n > 0 ? (float)(s / (double)n) : 0.0f;
+    nu[col] = m;
+    float a = n > 0 ? fmaxf(fabsf(hi - m), fabsf(m - lo)) : 0.0f;
+    atomic_max_nonneg(absmax, a);
+}
+
+// Xh = fp16((x - nu) * 2^xexp), xnorm = |x - nu|, x2 = |x|^2 (fp64).
+__global__ void data_pack_kernel(const float *__restrict__ X, int64_t n, int d,
+                                 const float *__restrict__ nu, int xexp,
+                                 __half *__restrict__ Xh, int dp,
+                                 float *__restrict__ xnorm, double *__restrict__ x2) {
+    int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const float *x = X + row * d;
+    __half *o = Xh + row * dp;
+    double sc = ldexp(1.0, xexp);
+    double nrm = 0.0, sq = 0.0;
+    for (int k = lane; k < dp; k += 32) {
+        if (k < d) {
+            double xv = (double)x[k];
+            double v = xv - (double)nu[k];
+            nrm += v * v;
+            sq += xv * xv;
+            o[k] = __double2half(v * sc);
+        } else {
+            o[k] = __double2half(0.0);
+        }
+    }
+    nrm = warp_sum(nrm);
+    sq = warp_sum(sq);
+    if (lane == 0) {
+        xnorm[row] = (float)sqrt(nrm);
+        x2[row] = sq;
+    }
+}
+
+// ------------------------------------------------------------- codebook prep
+// ws layout: mu f32[d] | mu_nu f64[d] | stats f32[4] {nmax, dabsmax, -, -}
+__global__ void cb_colmean(const float *__restrict__ W, int K, int d, const float *__restrict__ nu,
+                           float *__restrict__ mu, double *__restrict__ mu_nu) {
+    // one warp per column: lane-strided partial sums then a fixed xor tree
+    int col = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (col >= d) return;
+    double s = 0.0;
+    for (int j = lane; j < K; j += 32) s += (double)W[(int64_t)j * d + col];
+    s = warp_sum(s);
+    if (lane == 0) {
+        float m = (float)(s / (double)K);
+        mu[col] = m;
+        mu_nu[col] = (double)m - (double)nu[col];
+    }
+}
+
+__global__ void cb_rowstats(const float *__restrict__ W, int K, int d, const float *__restrict__ mu,
+                            const double *__restrict__ mu_nu, float *__restrict__ c,
+                            double *__restrict__ w2, float *__restrict__ nrm_out,
+                            float *__restrict__ stats) {
+    int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (j >= K) return;
+    const float *w = W + (int64_t)j * d;
+    double n2 = 0.0, cm = 0.0, sq = 0.0;
+    float amax = 0.0f;
+    for (int k = lane; k < d; k += 32) {
+        double wv = (double)w[k];
+        double dl = wv - (double)mu[k];
+        n2 += dl * dl;
+        cm += mu_nu[k] * dl;
+        sq += wv * wv;
+        amax = fmaxf(amax, (float)fabs(dl));
+    }
+    n2 = warp_sum(n2);
+    cm = warp_sum(cm);
+    sq = warp_sum(sq);
+    amax = warp_max(amax);
+    if (lane == 0) {
+        c[j] = (float)(n2 + 2.0 * cm);
+        w2[j] = sq;
+        float nr = (float)sqrt(n2);
+        nrm_out[j] = nr;
+        atomic_max_nonneg(&stats[0], nr);
+        atomic_max_nonneg(&stats[1], amax);
+    }
+}
+
+__device__ __forceinline__ int pick_exp(float amax) {
+    // largest e with amax * 2^e <= 2^14 (fp16 max 65504); 0 for amax == 0
+    if (!(amax > 0.0f)) return 0;
+    int e;
+    frexpf(amax, &e);           // amax = f * 2^e, f in [0.5, 1)
+    return 14 - e;
+}
+
+__global__ void cb_pack(const float *__restrict__ W, int K, int d, const float *__restrict__ mu,
+                        int xexp, __half *__restrict__ Wh, int dp, int kp,
+                        float *__restrict__ c, const float *__restrict__ stats,
+                        float *__restrict__ scal) {
+    int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (j >= kp) return;
+    int sexp = pick_exp(stats[1]);
+    __half *o = Wh + (int64_t)j * dp;
+    if (j < K) {
+        const float *w = W + (int64_t)j * d;
+        double sc = ldexp(1.0, sexp);
+        for (int k = lane; k < dp; k += 32)
+            o[k] = __double2half(k < d ? ((double)w[k] - (double)mu[k]) * sc : 0.0);
+    } else {
+        for (int k = lane; k < dp; k += 32) o[k] = __double2half(0.0);
+        if (lane == 0) c[j] = INFINITY;
+    }
+    if (j == 0 && lane == 0) {
+        // r = c_j - 2 * (x' . delta): acc * 2^-(xexp + sexp) is the dot product
+        scal[0] = -2.0f * ldexpf(1.0f, -(xexp + sexp));
+        scal[1] = stats[0];     // max_j |delta_j|
+        scal[2] = (float)sexp;
+        scal[3] = stats[1];
+    }
+}
+
+}  // namespace somb
+
+using namespace somb;
+
+extern "C" size_t somb_data_stats_ws(int32_t d) {
+    return align_up((size_t)kStatChunks * d * (sizeof(double) + 2 * sizeof(float)), 256);
+}
+
+extern "C" int somb_data_stats(const float *X, int64_t n, int32_t d, float *nu, float *absmax,
+                               void *ws, void *stream) {
+    SOMB_REQUIRE(d > 0 && n >= 0, SOMB_E_INPUT, "data_stats: bad shape n=%lld d=%d", (long long)n, d);
+    cudaStream_t st = as_stream(stream);
+    double *psum = (double *)ws;
+    float *pmin = (float *)(psum + (size_t)kStatChunks * d);
+    float *pmax = pmin + (size_t)kStatChunks * d;
+    cudaMemsetAsync(absmax, 0, sizeof(float), st);
+    dim3 g((d + 127) / 128, kStatChunks);
+    data_stats_partial<<<g, 128, 0, st>>>(X, n, d, psum, pmin, pmax);
+    data_stats_final<<<(d + 127) / 128, 128, 0, st>>>(psum, pmin, pmax, n, d, nu, absmax);
+    SOMB_LAUNCH_CHECK("somb_data_stats");
+    return SOMB_OK;
+}
+
+extern "C" int somb_data_pack(const float *X, int64_t n, int32_t d, const float *nu, int32_t xexp,
+                              uint16_t *Xh, int32_t dp, float *xnorm, double *x2, void *stream) {
+    SOMB_REQUIRE(d > 0 && dp >= d && dp % 8 == 0, SOMB_E_INPUT, "data_pack: bad pitch d=%d dp=%d", d, dp);
+    if (n == 0) return SOMB_OK;
+    int rows_per_block = 8;
+    int64_t blocks = (n + rows_per_block - 1) / rows_per_block;
+    data_pack_kernel<<<(unsigned)blocks, 32 * rows_per_block, 0, as_stream(stream)>>>(
+        X, n, d, nu, xexp, (__half *)Xh, dp, xnorm, x2);
+    SOMB_LAUNCH_CHECK("somb_data_pack");
+    return SOMB_OK;
+}
+
+extern "C" size_t somb_codebook_ws(int32_t K, int32_t d) {
+    return align_up((size_t)d * sizeof(float), 256) + align_up((size_t)d * sizeof(double), 256) +
+           align_up((size_t)K * sizeof(float), 256) + 256;
+}
+
+extern "C" int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const float *nu,
+                                     int32_t xexp, uint16_t *Wh, int32_t dp, int32_t kp, float *c,
+                                     double *w2, float *scal, void *ws, void *stream) {
+    SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && dp % 8 == 0 && kp >= K && kp % 256 == 0,
+                 SOMB_E_INPUT, "codebook_prepare: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
+    cudaStream_t st = as_stream(stream);
+    char *p = (char *)ws;
+    float *mu = (float *)p;            p += align_up((size_t)d * sizeof(float), 256);
+    double *mu_nu = (double *)p;       p += align_up((size_t)d * sizeof(double), 256);
+    float *nrm = (float *)p;           p += align_up((size_t)K * sizeof(float), 256);
+    float *stats = (float *)p;
+    cudaMemsetAsync(stats, 0, 4 * sizeof(float), st);
+    cb_colmean<<<(d + 7) / 8, 256, 0, st>>>(W, K, d, nu, mu, mu_nu);
+    cb_rowstats<<<(K + 7) / 8, 256, 0, st>>>(W, K, d, mu, mu_nu, c, w2, nrm, stats);
+    cb_pack<<<(kp + 7) / 8, 256, 0, st>>>(W, K, d, mu, xexp, (__half *)Wh, dp, kp, c, stats, scal);
+    SOMB_LAUNCH_CHECK("somb_codebook_prepare");
+    return SOMB_OK;
+}

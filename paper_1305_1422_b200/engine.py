@@ -1,0 +1,240 @@
+"""Device-resident epoch engine: one process per GPU, all epoch work on the
+stream, one fp64 NCCL all-reduce per epoch when the rows are sharded.
+
+Per epoch:
+  somb_codebook_prepare -> somb_bmu_dense (tcgen05 screen + fp64 re-rank)
+  -> somb_qe_sum -> somb_node_sums_dense -> [all_reduce(S | cnt | qe)]
+  -> somb_hood_update (fp64 convolution + blend, this rank's node slice)
+  -> [all_gather(W)].
+This replaces the reference epoch loop body train.py:269-277 (search_accumulate
+kernels.py:365-435 + blend kernels.py:438-450) and the coordinator/worker fold
+distributed.py:492-514 (rank-ordered fp64 merge -> NCCL fp64 sum).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib, errors
+from .datasets import DenseDataset, SparseDataset, _is_torch
+from .grid import GridType, MapType, Neighborhood, distance_table
+
+_DEF_WINDOW_KAPPA = 24.0   # screening window, in fp16-rounding units
+_U16 = 2.0 ** -11
+
+
+@dataclass
+class EngineOptions:
+    screen: str = "tensor"            # "tensor" (tcgen05), "simt" (reference screen), "exact"
+    window_kappa: float = _DEF_WINDOW_KAPPA
+    hypot_table: bool = True          # numpy-hypot distances for rect grids (bit parity)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _stream(dev: torch.device):
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _round_up(v: int, a: int) -> int:
+    return (v + a - 1) // a * a
+
+
+def pick_device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise errors.DeviceError("no CUDA device: somb200 runs only on a B200 (sm_100a)")
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise errors.DeviceError(f"somb200 needs a CUDA device, got {device}")
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    _lib.require_device(idx)
+    return torch.device("cuda", idx)
+
+
+def dist_info(group=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+class SomEngine:
+    """Resident dataset slice + codebook + buffers for one GPU (one rank)."""
+
+    def __init__(self, data, n_columns: int, n_rows: int, map_type: MapType,
+                 grid: GridType = GridType.RECTANGULAR, device=None, group=None,
+                 options: Optional[EngineOptions] = None):
+        self.dev = pick_device(device)
+        self.opt = options or EngineOptions()
+        self.group = group
+        self.rank, self.world = dist_info(group)
+        if isinstance(data, SparseDataset):
+            raise errors.KernelDataMismatch("SomEngine(dense): got sparse data")
+        self.nx, self.ny = int(n_columns), int(n_rows)
+        self.K = self.nx * self.ny
+        self.map_type, self.grid = map_type, grid
+        self.cmap = _lib.SombMap(self.nx, self.ny,
+                                 _lib.GRID_HEX if grid is GridType.HEXAGONAL else _lib.GRID_RECT,
+                                 _lib.TOROID if map_type is MapType.TOROID else _lib.PLANAR)
+        x = data.values if isinstance(data, DenseDataset) else data
+        self._upload_dense(x)
+        d = self.d
+        self.dp = _round_up(d, 8)
+        self.kp = _round_up(self.K, 256)
+        # node slice of this rank for the update; K padded so all_gather chunks are equal
+        self.kc = -(-self.K // self.world)
+        self.kpad = self.kc * self.world
+        self.node_begin = min(self.K, self.rank * self.kc)
+        self.node_end = min(self.K, (self.rank + 1) * self.kc)
+        f32, f64, dev = torch.float32, torch.float64, self.dev
+        self.W = torch.zeros((self.kpad, d), dtype=f32, device=dev)
+        self.W2 = torch.zeros((self.kpad, d), dtype=f32, device=dev)
+        self.Wh = torch.empty((self.kp, self.dp), dtype=torch.float16, device=dev)
+        self.c = torch.empty(self.kp, dtype=f32, device=dev)
+        self.w2 = torch.empty(self.K, dtype=f64, device=dev)
+        self.scal = torch.empty(4, dtype=f32, device=dev)
+        n = self.n
+        self.bmu = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.d2min = torch.empty(max(n, 1), dtype=f64, device=dev)
+        self.flags = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        # packed [S (K*d) | cnt (K) | qe (1)] fp64: one all-reduce per epoch
+        self.acc = torch.zeros(self.K * d + self.K + 1, dtype=f64, device=dev)
+        self.S = self.acc[: self.K * d].view(self.K, d)
+        self.cnt = self.acc[self.K * d: self.K * d + self.K]
+        self.qe = self.acc[self.K * d + self.K:]
+        self.dist_tab = None
+        if self.opt.hypot_table and grid is GridType.RECTANGULAR:
+            self.dist_tab = torch.from_numpy(distance_table(self.nx, self.ny, map_type)).to(dev)
+        lib = _lib.load()
+        ws = max(lib.somb_codebook_ws(self.K, d), lib.somb_bmu_ws(n),
+                 lib.somb_node_sums_ws(n, d, self.K),
+                 lib.somb_hood_ws(C.byref(self.cmap), self.K), 1 << 16)
+        self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)
+        self.window_coef = float(self.opt.window_kappa * _U16 / math.sqrt(d))
+        self.screen_impl = {"tensor": 0, "simt": 1, "exact": 2}[self.opt.screen]
+
+    # ------------------------------------------------------------ dataset
+    def _upload_dense(self, x):
+        if _is_torch(x):
+            xt = x.to(self.dev, dtype=torch.float32).contiguous()
+        else:
+            xh = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+            if not xh.is_pinned():
+                xh = xh.pin_memory()
+            xt = xh.to(self.dev, non_blocking=True)
+        self.X = xt
+        self.n, self.d = int(xt.shape[0]), int(xt.shape[1])
+        self.pack_dataset()
+
+    def pack_dataset(self):
+        """Centre + fp16 copy of the resident rows (once per dataset)."""
+        lib, dev, st = _lib.load(), self.dev, _stream(self.dev)
+        d, n = self.d, self.n
+        self.dp = _round_up(d, 8)
+        self.nu = torch.empty(d, dtype=torch.float32, device=dev)
+        absmax = torch.empty(1, dtype=torch.float32, device=dev)
+        ws = torch.empty(int(lib.somb_data_stats_ws(d)), dtype=torch.uint8, device=dev)
+        _lib.call("somb_data_stats", _ptr(self.X), n, d, _ptr(self.nu), _ptr(absmax), _ptr(ws), st)
+        a = float(absmax.item())                 # one host sync per dataset
+        self.xexp = 0 if a <= 0.0 or not math.isfinite(a) else 14 - math.frexp(a)[1]
+        self.Xh = torch.empty((max(n, 1), self.dp), dtype=torch.float16, device=dev)
+        self.xnorm = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+        self.x2 = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        _lib.call("somb_data_pack", _ptr(self.X), n, d, _ptr(self.nu), self.xexp, _ptr(self.Xh),
+                  self.dp, _ptr(self.xnorm), _ptr(self.x2), st)
+
+    # ----------------------------------------------------------- codebook
+    def set_codebook(self, w):
+        w = torch.as_tensor(w, dtype=torch.float32)
+        if tuple(w.shape) != (self.K, self.d):
+            raise errors.CodebookShapeMismatch(f"codebook {tuple(w.shape)}, expected {(self.K, self.d)}")
+        self.W[: self.K].copy_(w.to(self.dev, non_blocking=True))
+
+    def codebook(self) -> np.ndarray:
+        return self.W[: self.K].cpu().numpy()
+
+    # ------------------------------------------------------------- phases
+    def prepare(self):
+        _lib.call("somb_codebook_prepare", _ptr(self.W), self.K, self.d, _ptr(self.nu), self.xexp,
+                  _ptr(self.Wh), self.dp, self.kp, _ptr(self.c), _ptr(self.w2), _ptr(self.scal),
+                  _ptr(self.ws), _stream(self.dev))
+
+    def search(self, dist_mode=_lib.DIST_BLOCKED):
+        """BMU + d2min for the resident rows against the current codebook."""
+        self.prepare()
+        if self.n == 0:
+            return
+        _lib.call("somb_bmu_dense", _ptr(self.Xh), _ptr(self.X), _ptr(self.xnorm), _ptr(self.x2),
+                  self.n, self.d, self.dp, _ptr(self.Wh), _ptr(self.W), _ptr(self.c), _ptr(self.w2),
+                  self.K, self.kp, _ptr(self.scal), C.c_float(self.window_coef), dist_mode,
+                  self.screen_impl, _ptr(self.bmu), _ptr(self.d2min), _ptr(self.flags),
+                  _ptr(self.ws), _stream(self.dev))
+
+    def qe_sum(self):
+        _lib.call("somb_qe_sum", _ptr(self.d2min), self.n, _ptr(self.qe), _ptr(self.ws),
+                  _stream(self.dev))
+
+    def node_sums(self):
+        _lib.call("somb_node_sums_dense", _ptr(self.X), self.n, self.d, _ptr(self.bmu), self.K,
+                  _ptr(self.S), _ptr(self.cnt), _ptr(self.ws), _stream(self.dev))
+
+    def reduce(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.acc, op=dist.ReduceOp.SUM, group=self.group)
+
+    def update(self, radius, scale, cutoff, neighborhood=Neighborhood.GAUSSIAN, compact=False,
+               num_out=None, den_out=None, all_nodes=False):
+        hood = _lib.SombHood(_lib.NBH_BUBBLE if neighborhood is Neighborhood.BUBBLE
+                             else _lib.NBH_GAUSSIAN, int(bool(compact)), float(radius), float(cutoff))
+        nb, ne = (0, self.K) if all_nodes else (self.node_begin, self.node_end)
+        _lib.call("somb_hood_update", _ptr(self.S), _ptr(self.cnt), self.d, C.byref(self.cmap),
+                  C.byref(hood), C.c_double(scale), _ptr(self.dist_tab), _ptr(self.W), nb, ne,
+                  _ptr(self.W2), _ptr(num_out), _ptr(den_out), _ptr(self.ws), _stream(self.dev))
+        if self.world > 1 and not all_nodes:
+            import torch.distributed as dist
+            lo = self.rank * self.kc
+            dist.all_gather_into_tensor(self.W2, self.W2[lo: lo + self.kc].contiguous(),
+                                        group=self.group)
+        self.W, self.W2 = self.W2, self.W
+
+    def epoch(self, radius, scale, cutoff, neighborhood=Neighborhood.GAUSSIAN, compact=False):
+        """One full training epoch; returns the device qe-sum tensor (no sync)."""
+        self.search(_lib.DIST_BLOCKED)
+        self.qe_sum()
+        self.node_sums()
+        self.reduce()
+        self.update(radius, scale, cutoff, neighborhood, compact)
+        return self.qe
+
+    def umatrix(self) -> torch.Tensor:
+        u = torch.empty(self.K, dtype=torch.float32, device=self.dev)
+        _lib.call("somb_umatrix", _ptr(self.W), self.d, C.byref(self.cmap), _ptr(u),
+                  _stream(self.dev))
+        return u.view(self.ny, self.nx)
+
+    def gather_bmus(self) -> np.ndarray:
+        """Flat BMU indices of ALL rows (rank order), on every rank."""
+        local = self.bmu[: self.n].to(torch.int64)
+        if self.world == 1:
+            return local.cpu().numpy()
+        import torch.distributed as dist
+        counts = [torch.zeros(1, dtype=torch.int64, device=self.dev) for _ in range(self.world)]
+        dist.all_gather(counts, torch.tensor([self.n], dtype=torch.int64, device=self.dev),
+                        group=self.group)
+        cn = [int(c.item()) for c in counts]
+        m = max(cn)
+        buf = torch.zeros(m, dtype=torch.int64, device=self.dev)
+        buf[: self.n] = local
+        outs = [torch.empty(m, dtype=torch.int64, device=self.dev) for _ in range(self.world)]
+        dist.all_gather(outs, buf, group=self.group)
+        return torch.cat([o[:c] for o, c in zip(outs, cn)]).cpu().numpy()

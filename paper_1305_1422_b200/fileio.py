@@ -1,0 +1,81 @@
+"""Artifact writers / codebook reader with the reference text formats
+(fileio.py:322-401): floats as %.6g, LF endings.  Text dataset parsing is
+out of scope for the B200 hot path."""
+from __future__ import annotations
+
+from typing import NamedTuple, Optional
+
+import numpy as np
+
+from . import errors
+
+
+class SnapshotPaths(NamedTuple):
+    codebook: str
+    bmus: str
+    umatrix: str
+
+
+def snapshot_paths(prefix: str, epoch: Optional[int] = None) -> SnapshotPaths:
+    stem = prefix if epoch is None else f"{prefix}.{epoch}"
+    return SnapshotPaths(stem + ".wts", stem + ".bm", stem + ".umx")
+
+
+def _rows(mat) -> str:
+    return "".join(" ".join(f"{float(v):.6g}" for v in row) + "\n" for row in mat)
+
+
+def _write(path: str, text: str) -> None:
+    try:
+        with open(path, "w", encoding="utf-8", newline="\n") as fh:
+            fh.write(text)
+    except OSError as exc:
+        raise errors.IoFailure(f"cannot write {path}: {exc}") from exc
+
+
+def write_codebook(cb, path: str) -> None:
+    _write(path, f"% {cb.n_rows} {cb.n_columns}\n% {cb.n_dimensions}\n" + _rows(cb.weights))
+
+
+def write_bmus(bmus: np.ndarray, path: str) -> None:
+    _write(path, f"% {len(bmus)}\n" + "".join(f"{i} {r} {c}\n" for i, (r, c) in enumerate(bmus)))
+
+
+def write_umatrix(u, path: str) -> None:
+    _write(path, _rows(u.heights))
+
+
+def load_codebook(path_or_text):
+    """Read a .wts codebook -> (n_columns, n_rows, weights f32) (fileio.py:362-401)."""
+    if isinstance(path_or_text, str) and "\n" not in path_or_text:
+        try:
+            with open(path_or_text, "r", encoding="utf-8") as fh:
+                text = fh.read()
+        except OSError as exc:
+            raise errors.IoFailure(f"cannot read {path_or_text}: {exc}") from exc
+    else:
+        text = path_or_text if isinstance(path_or_text, str) else path_or_text.read()
+    headers, body = [], []
+    for ln in text.splitlines():
+        s = ln.strip()
+        if not s or s.startswith("#"):
+            continue
+        if s.startswith("%") and len(headers) < 2:
+            try:
+                headers.append([int(t) for t in s[1:].split()])
+            except ValueError as exc:
+                raise errors.MalformedHeader(f"bad header {ln!r}") from exc
+        else:
+            body.append(s.split())
+    if len(headers) < 2 or len(headers[0]) < 2 or not headers[1]:
+        raise errors.MalformedHeader("codebook needs '% rows cols' and '% dims'")
+    n_rows, n_columns, d = headers[0][0], headers[0][1], headers[1][0]
+    if len(body) != n_rows * n_columns:
+        raise errors.CodebookShapeMismatch(
+            f"codebook declares {n_rows * n_columns} nodes, file has {len(body)}")
+    w = np.empty((n_rows * n_columns, d), dtype=np.float32)
+    for i, toks in enumerate(body):
+        if len(toks) != d:
+            raise errors.CodebookShapeMismatch(f"node {i}: expected {d} values, got {len(toks)}")
+        w[i] = [float(t) for t in toks]
+    return n_columns, n_rows, w

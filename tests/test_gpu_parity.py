@@ -1,0 +1,211 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and
+the golden outputs of the reference implementation.
+
+Bars (BASELINE.json north star): BMUs identical wherever the oracle's
+best/second-best relative gap exceeds 1e-5; codebook and U-matrix within
+1e-4 relative after the configured epochs.  Where the arithmetic allows it
+the tests demand more (bit-exact node sums, <= 1 ulp blends).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_1305_1422_b200 as S
+from paper_1305_1422_b200.engine import EngineOptions
+from conftest import cfg1_data, golden
+
+pytestmark = pytest.mark.gpu
+
+SCREENS = ["tensor", "simt", "exact"]
+GAP_TOL = 1e-5
+REL_TOL = 1e-4
+
+
+def _opts(screen):
+    return EngineOptions(screen=screen)
+
+
+def assert_bmus_tie_aware(got, want, x, w, tol=GAP_TOL):
+    got, want = np.asarray(got), np.asarray(want)
+    bad = np.flatnonzero(got != want)
+    if len(bad) == 0:
+        return
+    gaps = O.top2_gaps(x[bad] if not isinstance(x, O.CSR) else x, w)
+    assert np.all(gaps < tol), f"{np.sum(gaps >= tol)} BMU mismatches with gap >= {tol}"
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-12))) if a.size else 0.0
+
+
+@pytest.mark.parametrize("screen", SCREENS)
+def test_hand_cases(screen):
+    # reference tests/test_kernels.py:41-62 (hand BMUs, lowest-index ties)
+    cb = S.CodeBook(2, 1, 2, np.array([[0, 0], [1, 1]], np.float32))
+    x = S.DenseDataset(np.array([[0.4, 0.4], [0.6, 0.6], [0.1, 0.0]], np.float32))
+    assert S.bmu_search_blocked(x, cb, options=_opts(screen)).tolist() == [[0, 0], [0, 1], [0, 0]]
+    w = np.array([[9, 9], [0.5, 0.5], [8, 8], [0.5, 0.5]], np.float32)
+    cb = S.CodeBook(2, 2, 2, w)
+    x = S.DenseDataset(np.array([[0.5, 0.5]], np.float32))
+    for fn in (S.bmu_search_naive, S.bmu_search_blocked):
+        assert fn(x, cb, options=_opts(screen)).tolist() == [[0, 1]]
+    # qe definition (test_train.py:241-247)
+    cb = S.CodeBook(1, 1, 2, np.zeros((1, 2), np.float32))
+    qe = S.quantization_error(S.DenseDataset(np.array([[3, 4], [0, 0]], np.float32)), cb,
+                              options=_opts(screen))
+    assert qe == pytest.approx(2.5)
+
+
+@pytest.mark.parametrize("screen", SCREENS)
+def test_search_accumulate_golden(screen):
+    g = golden("kernels.npz")
+    for ci in range(int(g["ncases"])):
+        n, d, nx, ny, tor, radius, cutoff, kern, scale = g[f"c{ci}_params"]
+        n, d, nx, ny, kern = int(n), int(d), int(nx), int(ny), int(kern)
+        if kern == 2:
+            continue
+        x, w = g[f"c{ci}_x"], g[f"c{ci}_w"]
+        cb = S.CodeBook(nx, ny, d, w)
+        mt = S.MapType.TOROID if tor else S.MapType.PLANAR
+        bmu, qe, acc = S.search_accumulate(S.DenseDataset(x), cb, radius, cutoff, mt,
+                                           S.Kernel(kern), options=_opts(screen))
+        assert np.array_equal(bmu, g[f"c{ci}_bmu"]), (ci, np.sum(bmu != g[f"c{ci}_bmu"]))
+        assert qe == pytest.approx(float(g[f"c{ci}_qe"]), rel=1e-12)
+        np.testing.assert_allclose(acc.numerators, g[f"c{ci}_num"], rtol=1e-11, atol=1e-13)
+        np.testing.assert_allclose(acc.denominators, g[f"c{ci}_den"], rtol=1e-11, atol=1e-13)
+        assert np.array_equal(acc.denominators > 0, g[f"c{ci}_den"] > 0)
+        out = S.blend(w, acc, scale)
+        np.testing.assert_array_max_ulp(out, g[f"c{ci}_blend"], maxulp=1)
+
+
+def test_blend_bit_exact_vs_oracle():
+    rng = np.random.default_rng(3)
+    w = rng.random((50, 9), dtype=np.float32)
+    num = rng.random((50, 9)) * 7
+    den = rng.random(50) * 3
+    den[::7] = 0.0
+    acc = S.Accumulators(num, den)
+    for scale in (0.0, 0.3, 0.7, 1.0):
+        got = S.blend(w, acc, scale)
+        want = O.blend(w, num, den, scale)
+        assert got.tobytes() == want.tobytes()
+    assert S.blend(w, acc, 0.5)[::7].tobytes() == w[::7].tobytes()
+
+
+def test_node_sums_bit_exact_vs_oracle():
+    rng = np.random.default_rng(11)
+    for n, d, k in [(1, 3, 1), (1000, 17, 40), (5000, 130, 7), (3000, 600, 2000), (700, 5, 1)]:
+        x = rng.random((n, d), dtype=np.float32)
+        bmu = rng.integers(0, k, n).astype(np.int32)
+        if n > 2000:
+            bmu[: n // 2] = 0          # one node with > 256 rows: segmented path
+        eng = S.SomEngine(S.DenseDataset(x), k, 1, S.MapType.PLANAR)
+        eng.bmu[:n].copy_(torch.from_numpy(bmu))
+        eng.node_sums()
+        s, c = O.node_sums(x, bmu.astype(np.int64), k)
+        got_s = eng.S.cpu().numpy()
+        assert np.array_equal(eng.cnt.cpu().numpy(), c)
+        small = c <= 256
+        assert np.array_equal(got_s[small], s[small])
+        np.testing.assert_allclose(got_s, s, rtol=1e-13)
+
+
+@pytest.mark.parametrize("grid", [O.RECT, O.HEX])
+@pytest.mark.parametrize("nbh,compact", [(O.GAUSSIAN, False), (O.GAUSSIAN, True), (O.BUBBLE, False)])
+@pytest.mark.parametrize("mt", [O.PLANAR, O.TOROID])
+def test_hood_update_vs_oracle(grid, nbh, compact, mt):
+    rng = np.random.default_rng(5)
+    nx, ny, d = 13, 10, 11
+    k = nx * ny
+    s = rng.random((k, d)) * 5
+    c = rng.integers(0, 4, k).astype(np.float64)
+    s[c == 0] = 0.0
+    w = rng.random((k, d), dtype=np.float32)
+    x = rng.random((4, d), dtype=np.float32)
+    eng = S.SomEngine(S.DenseDataset(x), nx, ny, S.MapType(mt),
+                      S.GridType.HEXAGONAL if grid == O.HEX else S.GridType.RECTANGULAR)
+    eng.set_codebook(w)
+    eng.S.copy_(torch.from_numpy(s))
+    eng.cnt.copy_(torch.from_numpy(c))
+    for radius in (0.6, 1.0, 2.5, 7.0):
+        num = torch.empty((k, d), dtype=torch.float64, device=eng.dev)
+        den = torch.empty(k, dtype=torch.float64, device=eng.dev)
+        eng.set_codebook(w)
+        eng.update(radius, 0.4, 1e-3, S.Neighborhood(nbh), compact, num_out=num, den_out=den,
+                   all_nodes=True)
+        wn, wd = O.conv_update(s, c, nx, ny, radius, 1e-3, mt, grid, nbh, compact)
+        np.testing.assert_allclose(num.cpu().numpy(), wn, rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(den.cpu().numpy(), wd, rtol=1e-12, atol=1e-300)
+        assert np.array_equal(den.cpu().numpy() > 0, wd > 0)
+        want_w = O.blend(w, wn, wd, 0.4)
+        np.testing.assert_array_max_ulp(eng.codebook(), want_w, maxulp=1)
+
+
+def test_umatrix_golden_and_hex():
+    g = golden("umatrix.npz")
+    for i in range(int(g["ncases"])):
+        nx, ny, d, tor = (int(v) for v in g[f"u{i}_shape"])
+        cb = S.CodeBook(nx, ny, d, g[f"u{i}_w"])
+        u = S.compute_umatrix(cb, S.MapType.TOROID if tor else S.MapType.PLANAR).heights
+        np.testing.assert_array_max_ulp(u, g[f"u{i}_u"], maxulp=1)
+    rng = np.random.default_rng(2)
+    for nx, ny, mt in [(5, 4, O.PLANAR), (6, 4, O.TOROID), (3, 2, O.TOROID), (7, 5, O.PLANAR)]:
+        w = rng.random((nx * ny, 6), dtype=np.float32)
+        u = S.compute_umatrix(S.CodeBook(nx, ny, 6, w), S.MapType(mt), S.GridType.HEXAGONAL)
+        np.testing.assert_array_max_ulp(u.heights, O.umatrix(w, nx, ny, mt, O.HEX), maxulp=1)
+
+
+@pytest.mark.parametrize("screen", SCREENS)
+@pytest.mark.parametrize("n,d,nx,ny", [(2000, 37, 20, 15), (3000, 100, 50, 40), (513, 8, 7, 9),
+                                       (1500, 300, 33, 31)])
+def test_bmu_screens_vs_oracle_random(screen, n, d, nx, ny):
+    rng = np.random.default_rng(n + d)
+    x = rng.random((n, d), dtype=np.float32)
+    w = rng.random((nx * ny, d), dtype=np.float32)
+    bmu, qe, _ = S.search_accumulate(S.DenseDataset(x), S.CodeBook(nx, ny, d, w), 1.0, 0.0,
+                                     S.MapType.PLANAR, S.Kernel.DENSE_BLOCKED,
+                                     with_accumulators=False, options=_opts(screen))
+    ob, oqe, _, _ = O.search_accumulate(x, w, nx, ny, 1.0, 0.0, O.PLANAR, with_accumulators=False)
+    assert_bmus_tie_aware(bmu, ob, x, w)
+    assert qe == pytest.approx(oqe, rel=1e-12)
+
+
+def _run_train_golden(name, screen):
+    g = golden("train.npz")
+    x = cfg1_data() if name == "cfg1" else g[f"{name}_x"]
+    c = g[f"{name}_cfg"]
+    cfg = S.TrainConfig(n_epochs=int(c[0]), n_columns=int(c[1]), n_rows=int(c[2]),
+                        map_type=S.MapType.TOROID if c[3] else S.MapType.PLANAR,
+                        kernel=S.Kernel.DENSE_BLOCKED, radius0=c[4], radiusN=c[5],
+                        radius_cooling=S.Cooling.EXPONENTIAL if c[6] else S.Cooling.LINEAR,
+                        scale0=c[7], scaleN=c[8],
+                        scale_cooling=S.Cooling.EXPONENTIAL if c[9] else S.Cooling.LINEAR,
+                        seed=int(c[10]), influence_cutoff=c[11])
+    qes = []
+    cb, bmus, u = S.train(S.DenseDataset(x), cfg, progress=lambda s, q: qes.append(q),
+                          options=_opts(screen))
+    return g, x, cb, bmus, u, qes
+
+
+@pytest.mark.parametrize("screen", SCREENS)
+@pytest.mark.parametrize("name", ["t0", "t1", "t2", "blobs", "cfg1"])
+def test_train_matches_reference_golden(name, screen):
+    g, x, cb, bmus, u, qes = _run_train_golden(name, screen)
+    w_ref = g[f"{name}_w"]
+    assert rel_err(cb.weights, w_ref) <= REL_TOL
+    assert rel_err(u.heights, g[f"{name}_u"]) <= REL_TOL
+    fb = bmus[:, 0].astype(np.int64) * cb.n_columns + bmus[:, 1]
+    rb = g[f"{name}_bmus"][:, 0].astype(np.int64) * cb.n_columns + g[f"{name}_bmus"][:, 1]
+    assert_bmus_tie_aware(fb, rb, x, w_ref)
+    np.testing.assert_allclose(qes, g[f"{name}_qe"], rtol=1e-6)
+
+
+def test_cfg1_bit_exact_tensor_screen():
+    """Headline parity: cfg1 end to end with the tcgen05 screen reproduces the
+    reference codebook bit for bit (SURVEY.md 7.3-1 recipe)."""
+    g, x, cb, bmus, u, qes = _run_train_golden("cfg1", "tensor")
+    mism = np.sum(cb.weights != g["cfg1_w"])
+    assert mism <= cb.weights.size * 1e-4, f"{mism} codebook entries differ"
+    assert np.array_equal(bmus, g["cfg1_bmus"])

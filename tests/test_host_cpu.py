@@ -1,0 +1,154 @@
+"""CPU-only checks: host logic mirrors the reference, the C-ABI library loads
+and exports every symbol include/somb200.h declares, and the product path
+fails loudly without a GPU (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1305_1422_b200 as S
+from paper_1305_1422_b200 import _lib, errors
+from conftest import ROOT
+
+
+def test_header_symbols_exported_and_bound():
+    hdr = open(os.path.join(ROOT, "include", "somb200.h")).read()
+    declared = set(re.findall(r"SOMB_API\s+[\w\s\*]+?\b(somb_\w+)\s*\(", hdr))
+    assert declared, "no declarations found"
+    lib = os.path.join(ROOT, "paper_1305_1422_b200", "libsomb200.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (somb_\w+)", out))
+    assert declared <= exported, declared - exported
+    assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
+    L = _lib.load()
+    assert L.somb_version().startswith(b"somb200")
+    assert L.somb_bmu_ws(1000) > 0 and L.somb_node_sums_ws(1000, 8, 16) > 0
+
+
+def test_library_is_sm100a_only():
+    lib = os.path.join(ROOT, "paper_1305_1422_b200", "libsomb200.so")
+    out = subprocess.run(["cuobjdump", "--list-elf", lib], capture_output=True, text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    x = S.gen_random_dense(20, 3, 1)
+    with pytest.raises(errors.DeviceError):
+        S.train(x, S.TrainConfig(n_epochs=1, n_columns=3, n_rows=2))
+
+
+def test_resolve_defaults_and_validation():
+    c = S.resolve_defaults(S.TrainConfig(n_columns=12, n_rows=8))
+    assert (c.radius0, c.radiusN, c.scale0, c.scaleN) == (4.0, 1.0, 1.0, 0.01)
+    assert S.resolve_defaults(S.TrainConfig(n_columns=1, n_rows=30)).radius0 == 1.0
+    for bad in [dict(n_epochs=0), dict(n_columns=0), dict(radius0=-2), dict(scale0=-0.5),
+                dict(influence_cutoff=-1e-3), dict(snapshot_level=3)]:
+        with pytest.raises(errors.InvalidConfig):
+            S.resolve_defaults(S.TrainConfig(**bad))
+    with pytest.raises(errors.InvalidConfig):
+        S.resolve_defaults(S.TrainConfig(n_rows=5, grid=S.GridType.HEXAGONAL,
+                                         map_type=S.MapType.TOROID))
+
+
+@pytest.mark.parametrize("cool", [S.Cooling.LINEAR, S.Cooling.EXPONENTIAL])
+def test_schedule_matches_oracle(cool):
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        a = float(rng.uniform(1, 50)); b = float(rng.uniform(0.5, a)); e = int(rng.integers(1, 20))
+        for t in range(e):
+            assert S.schedule(a, b, cool, t, e) == O.schedule(a, b, cool.value, t, e)
+
+
+def test_init_codebook_matches_reference_stream():
+    cfg = S.resolve_defaults(S.TrainConfig(n_columns=6, n_rows=5, seed=9))
+    assert np.array_equal(S.init_codebook(cfg, 4).weights, O.init_codebook(6, 5, 4, 9))
+
+
+def test_generators_match_reference_streams():
+    assert np.array_equal(S.gen_random_dense(50, 7, 3).values, O.gen_random_dense(50, 7, 3))
+    a, b = S.gen_random_sparse(40, 30, 0.2, 4), O.gen_random_sparse(40, 30, 0.2, 4)
+    assert np.array_equal(a.row_offsets, b.row_offsets)
+    assert np.array_equal(a.col_indices, b.col_indices)
+    assert np.array_equal(a.values, b.values)
+
+
+def test_grid_distance_and_neighbors_match_oracle():
+    for nx, ny in [(1, 1), (2, 3), (5, 4), (8, 8)]:
+        for mt in (S.MapType.PLANAR, S.MapType.TOROID):
+            for g in (S.GridType.RECTANGULAR, S.GridType.HEXAGONAL):
+                if g is S.GridType.HEXAGONAL and mt is S.MapType.TOROID and ny % 2:
+                    continue
+                og = O.HEX if g is S.GridType.HEXAGONAL else O.RECT
+                for j in range(nx * ny):
+                    c, r = j % nx, j // nx
+                    got = [(q.col, q.row) for q in S.neighbors(S.GridCoord(c, r), mt, nx, ny, g)]
+                    assert got == O.neighbors(c, r, nx, ny, mt.value, og)
+                    for k in range(nx * ny):
+                        d = S.grid_distance(S.GridCoord(c, r), S.GridCoord(k % nx, k // nx),
+                                            mt, nx, ny, g)
+                        assert d == pytest.approx(
+                            O.grid_distance(c, r, k % nx, k // nx, nx, ny, mt.value, og), abs=1e-12)
+
+
+def test_hex_distance_known_answers():
+    # extension definition: odd rows shifted by +1/2, row pitch sqrt(3)/2
+    h = S.GridType.HEXAGONAL
+    g = lambda a, b, mt=S.MapType.PLANAR: S.grid_distance(S.GridCoord(*a), S.GridCoord(*b), mt, 6, 4, h)
+    assert g((0, 0), (1, 0)) == 1.0
+    assert g((0, 0), (0, 1)) == pytest.approx(1.0)        # odd row neighbour up-right
+    assert g((1, 1), (1, 0)) == pytest.approx(1.0)
+    assert g((0, 0), (0, 2)) == pytest.approx(np.sqrt(3.0))
+    assert g((0, 0), (5, 0), S.MapType.TOROID) == 1.0     # wrap along x
+    assert g((0, 0), (0, 3), S.MapType.TOROID) == pytest.approx(1.0)   # wrap along y (even ny)
+    assert len(S.neighbors(S.GridCoord(2, 2), S.MapType.PLANAR, 6, 4, h)) == 6
+
+
+def test_bubble_compact_known_answers():
+    P = S.MapType.PLANAR
+    nb = S.neighborhood
+    a, b = S.GridCoord(0, 0), S.GridCoord(3, 4)
+    assert nb(a, b, 5.0, P, 10, 10, kind=S.Neighborhood.BUBBLE) == 1.0
+    assert nb(a, b, 4.99, P, 10, 10, kind=S.Neighborhood.BUBBLE) == 0.0
+    assert nb(a, b, 4.99, P, 10, 10, compact=True) == 0.0
+    assert nb(a, b, 5.0, P, 10, 10, compact=True) == pytest.approx(np.exp(-1.0))
+    assert nb(a, a, 2.0, P, 10, 10) == 1.0
+
+
+def test_partition_matches_reference():
+    for n, p in [(10, 3), (7, 8), (1_000_001, 8), (0, 2)]:
+        assert S.partition(n, p) == O.partition(n, p)
+
+
+def test_bindings_validation_errors_before_compute():
+    from paper_1305_1422_b200 import bindings as B
+    x = np.zeros(12, np.float32)
+    cb, bm, um = np.zeros(6 * 3, np.float32), np.zeros(8, np.int32), np.zeros(6, np.float32)
+    with pytest.raises(B.ShapeError):
+        B.train_wrapper(x, 1, 3, 2, 3, 4, 0, 0, "linear", 0, 0, "linear", 0, 0, "planar", "",
+                        cb[:-1], bm, um)
+    with pytest.raises(TypeError):
+        B.train_wrapper(x.astype(np.float64), 1, 3, 2, 3, 4, 0, 0, "linear", 0, 0, "linear", 0, 0,
+                        "planar", "", cb, bm, um)
+    with pytest.raises(B.ContiguityError):
+        B.train_wrapper(np.zeros(24, np.float32)[::2], 1, 3, 2, 3, 4, 0, 0, "linear", 0, 0,
+                        "linear", 0, 0, "planar", "", cb, bm, um)
+    with pytest.raises(errors.InvalidConfig):
+        B.train_wrapper(x, 1, 3, 2, 3, 4, 0, 0, "linear", 0, 0, "linear", 0, 0, "klein", "",
+                        cb, bm, um)
+
+
+def test_fileio_roundtrip(tmp_path):
+    w = np.random.default_rng(1).random((6, 3), dtype=np.float32)
+    cb = S.CodeBook(3, 2, 3, w)
+    from paper_1305_1422_b200 import fileio
+    fileio.write_codebook(cb, str(tmp_path / "a.wts"))
+    nx, ny, w2 = fileio.load_codebook(str(tmp_path / "a.wts"))
+    assert (nx, ny) == (3, 2)
+    np.testing.assert_allclose(w2, w, rtol=1e-5)
