@@ -83,20 +83,26 @@ screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __hal
 __global__ void rerank_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n,
                               int d, const float *__restrict__ W, const double *__restrict__ w2,
                               int K, const int *__restrict__ cand, const int *__restrict__ ccount,
-                              int dist_mode, int all, int *__restrict__ bmu,
+                              int dist_mode, int all, int split, int *__restrict__ bmu,
                               double *__restrict__ d2min) {
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
     const float *x = X + row * d;
-    int cnt = all ? K : ccount[row];
+    // candidate list: one segment [0, cc) or, for the two-half tcgen05
+    // epilogue, [0, cc & 255) and [CAP/2, CAP/2 + (cc >> 8 & 255))
+    int cc = all ? 0 : ccount[row];
+    int c0 = split ? (cc & 255) : cc;
+    int c1 = split ? ((cc >> 8) & 255) : 0;
+    int cnt = c0 + c1;
     bool scan_all = all || cnt <= 0;
     if (scan_all) cnt = K;
     double best = INFINITY;
-    int bestj = 0;
+    int bestj = 0x7fffffff;
     const double xx = x2[row];
     for (int q = 0; q < cnt; ++q) {
-        int j = scan_all ? q : cand[row * SOMB_CAND_CAP + q];
+        int j = scan_all ? q : cand[row * SOMB_CAND_CAP + (q < c0 ? q : SOMB_CAND_CAP / 2 + (q - c0))];
+        if ((unsigned)j >= (unsigned)K) continue;
         const float *w = W + (int64_t)j * d;
         double d2;
         if (dist_mode == SOMB_DIST_NAIVE) {
@@ -114,7 +120,7 @@ __global__ void rerank_kernel(const float *__restrict__ X, const double *__restr
             d2 = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, s), xx), w2[j]);
             d2 = fmax(d2, 0.0);
         }
-        if (d2 < best) {   // ascending j: strict < keeps the first minimum
+        if (d2 < best || (d2 == best && j < bestj)) {   // first minimum (lowest index)
             best = d2;
             bestj = j;
         }
@@ -180,8 +186,9 @@ extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *x
     cudaStream_t st = as_stream(stream);
     int *cand = (int *)ws;
     int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
-    int all = 0;
+    int all = 0, split = 0;
     if (screen_impl == 0) {
+        split = 1;
         int rc = launch_screen_tc((const __half *)Xh, n, dp, (const __half *)Wh, kp, c, xnorm, scal,
                                   window_coef, cand, ccount, flags, st);
         if (rc != SOMB_OK) return rc;
@@ -197,7 +204,7 @@ extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *x
     }
     const int wpb = 8;
     rerank_kernel<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
-        X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, bmu, d2min);
+        X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, split, bmu, d2min);
     SOMB_LAUNCH_CHECK("rerank");
     return SOMB_OK;
 }

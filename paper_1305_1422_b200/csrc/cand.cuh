@@ -13,6 +13,8 @@
 // set (rerank kernel) picks the BMU with first-minimum ties
 // (kernels.py:27-28, 203).
 #pragma once
+#include <float.h>
+
 #include "common.cuh"
 
 namespace somb {
@@ -26,9 +28,11 @@ struct CandRow {
 
 template <int CAP>
 __device__ __forceinline__ void cand_init(CandRow<CAP> &s, float win) {
-    s.rmin = INFINITY;
-    s.thr = INFINITY;
-    s.capbelow = INFINITY;
+    // finite start: screened values of padding / masked nodes are +inf and
+    // must never enter the set
+    s.rmin = FLT_MAX;
+    s.thr = FLT_MAX;
+    s.capbelow = FLT_MAX;
     s.win = win;
     s.cnt = 0;
     s.trunc = 0;
