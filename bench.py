@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the batch-SOM epoch hot path (driver contract).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config cfg2|cfg1|cfg4|cfg5]
+
+A step is one training epoch (tcgen05 BMU screen + fp64 re-rank + node sums
++ [NCCL all-reduce] + fp64 neighbourhood convolution + blend) over the whole
+synthetic dataset of the config, following the config's 10-epoch radius/scale
+schedule (step s runs epoch s mod 10).  Default workload: BASELINE cfg2 --
+200x200 toroid (K = 40,000), 1M x 1000 fp32, rows sharded over the N ranks
+(strong scaling).  `value` = N_rows * K / epoch time (BMU distance
+evaluations per second, whole job); X (4 GB) exceeds L2, so no flush is needed.
+
+--impl reference times the CPU path of the reference algorithm (the numpy
+oracle port, all host cores) on a bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n_rows, d, nx, ny, map, grid, neighborhood, compact, description)
+    "cfg1": (10_000, 100, 50, 40, "planar", "rectangular", "gaussian", False,
+             "cfg1: dense 50x40 planar rect map, 10k x 100 fp32 uniform, gaussian"),
+    "cfg2": (1_000_000, 1000, 200, 200, "toroid", "rectangular", "gaussian", False,
+             "cfg2: emergent 200x200 toroid, 1M x 1000 fp32 uniform, gaussian"),
+    "cfg4": (2_000_000, 256, 300, 300, "toroid", "hexagonal", "bubble", True,
+             "cfg4: hexagonal toroid 300x300, 2M x 256 fp32 uniform, bubble, compact support"),
+    "cfg5": (4_000_000, 128, 500, 500, "planar", "rectangular", "gaussian", False,
+             "cfg5: large emergent 500x500 planar, 4M x 128 fp32 uniform, gaussian"),
+}
+METRIC = "epoch time & BMU dist-evals/s (N·K·D) at 1/2/4/8 B200, % of roofline"
+UNIT = "dist-evals/s"
+N_EPOCHS = 10
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def schedule_for(cfg_name, epoch):
+    n, d, nx, ny, *_ = CONFIGS[cfg_name]
+    r0 = max(min(nx, ny) / 2.0, 1.0)
+    e = epoch % N_EPOCHS
+    frac = e / (N_EPOCHS - 1)
+    radius = r0 + (1.0 - r0) * frac if 0 < e < N_EPOCHS - 1 else (r0 if e == 0 else 1.0)
+    scale = 1.0 + (0.01 - 1.0) * frac if 0 < e < N_EPOCHS - 1 else (1.0 if e == 0 else 0.01)
+    return radius, scale
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def init_dist(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def cpu_reference_rate(cfg_name, n_sub, steps, warmup, seed=1001):
+    """Oracle port (numpy restatement of the reference path, kernels.py:365-450)
+    on all host cores: search_accumulate(DENSE_BLOCKED) over an n_sub-row
+    sample plus the full-codebook blend; the epoch time at full N is
+    (N / n_sub) * t_search_accumulate + t_blend (cost is linear in N,
+    SURVEY.md 8d)."""
+    import numpy as np
+    import oracle as O
+    n, d, nx, ny, mt, grid, nbh, compact, _ = CONFIGS[cfg_name]
+    rng = np.random.default_rng(seed)
+    x = rng.random((n_sub, d), dtype=np.float32)
+    w = O.init_codebook(nx, ny, d, 1)
+    og = O.HEX if grid == "hexagonal" else O.RECT
+    workers = os.cpu_count() or 1
+    t_sa, t_bl = [], []
+    for s in range(warmup + steps):
+        radius, scale = schedule_for(cfg_name, s)
+        t0 = time.perf_counter()
+        _, _, num, den = O.search_accumulate(x, w, nx, ny, radius, 1e-3, mt, O.DENSE_BLOCKED, workers,
+                                             True, og, nbh, compact)
+        t1 = time.perf_counter()
+        w = O.blend(w, num, den, scale)
+        t2 = time.perf_counter()
+        t_sa.append(t1 - t0)
+        t_bl.append(t2 - t1)
+    k = slice(warmup, None) if steps else slice(None)
+    sa, bl = statistics.median(t_sa[k]), statistics.median(t_bl[k])
+    t_epoch = (n / n_sub) * sa + bl
+    return {"value": n * nx * ny / t_epoch, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": f"{n_sub} of {n} rows x {nx * ny} nodes x {d} dims: search_accumulate "
+                      f"(DENSE_BLOCKED, {workers} workers) {sa:.2f} s + blend {bl:.2f} s per step, "
+                      f"median of {len(t_sa[k])}; epoch = N/n_sub * search + blend",
+            "seconds_per_step": t_epoch}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n, d, nx, ny, *_ , desc = CONFIGS[args.config]
+    n_sub = args.ref_rows
+    cb = cpu_reference_rate(args.config, n_sub, args.steps, args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["seconds_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic uniform [0,1) fp32 (numpy default_rng seed 1001), bounded row sample",
+            "config": {"workload": desc, "rows_sampled": n_sub, "K": nx * ny, "d": d},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    rank, world, local = init_dist(args)
+    import paper_1305_1422_b200 as S
+    from paper_1305_1422_b200 import _lib
+    from paper_1305_1422_b200.engine import EngineOptions, SomEngine
+    n, d, nx, ny, mt, grid, nbh, compact, desc = CONFIGS[args.config]
+    K = nx * ny
+    dev = torch.device("cuda", torch.cuda.current_device())
+    first, count = S.partition(n, world)[rank]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1001 + rank)
+    X = torch.rand((count, d), generator=gen, device=dev, dtype=torch.float32)
+    opts = EngineOptions(screen=args.screen)
+    mtype, gtype, nb = S.MapType(mt), S.GridType(grid), S.Neighborhood(nbh)
+    eng = SomEngine(X, nx, ny, mtype, gtype, device=dev, options=opts)
+    w0 = S.init_codebook(S.TrainConfig(n_columns=nx, n_rows=ny, seed=1), d).weights
+    eng.set_codebook(w0)
+    lib = _lib.load()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier(device_ids=[local])
+
+    for s in range(args.warmup):
+        r, sc = schedule_for(args.config, s)
+        eng.epoch(r, sc, 1e-3, nb, compact)
+    torch.cuda.synchronize()
+    barrier()
+    eng.timing = {}
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = lib.somb_launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    t_start.record()
+    for s in range(args.warmup, args.warmup + args.steps):
+        r, sc = schedule_for(args.config, s)
+        eng.epoch(r, sc, 1e-3, nb, compact)
+    t_end.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = lib.somb_launch_count() - l0
+    clk = clocks.stop()
+    elapsed = t_start.elapsed_time(t_end) / 1e3
+    phase_ms = {k: [a.elapsed_time(b) for a, b in v] for k, v in eng.timing.items()}
+    eng.timing = None
+    tmax = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    elapsed = float(tmax.item())
+    ms_step = elapsed * 1e3 / max(args.steps, 1)
+    value = n * K / (elapsed / max(args.steps, 1))
+
+    # roofline of the dominant kernel: the tcgen05 screen, algorithmic 2*n*K*d flops
+    pk, pk_kind = peaks()
+    scr = phase_ms.get("screen", [])
+    scr_ms = statistics.mean(scr) if scr else float("nan")
+    flops = 2.0 * count * K * d
+    achieved = flops / (scr_ms / 1e3) / 1e12
+    peak_sus = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_screen_{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "screen_tc_kernel (tcgen05 kind::f16)",
+                "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
+                "peak_kind": f"{pk_kind} bf16 dense sustained (fp16 kind::f16 runs at the bf16 rate)",
+                "frac_of_burst": achieved / pk.get("bf16_tflops", peak_sus),
+                "traffic": traffic, "flops_per_launch": flops, "avg_launch_ms": scr_ms}
+
+    # per-phase breakdown (rank-local averages)
+    phases = {k: statistics.mean(v) for k, v in phase_ms.items() if v}
+    flags = eng.flags[: eng.n].cpu().numpy()
+    trunc = float(((flags & 0xFF) | ((flags >> 8) & 0xFF)).astype(bool).mean()) if eng.n else 0.0
+
+    # end to end through the public API: host (pinned) data -> train() -> host results
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.empty((count, d), dtype=torch.float32, pin_memory=True)
+        Xh.copy_(X)
+        del eng
+        torch.cuda.empty_cache()
+        cfg = S.TrainConfig(n_epochs=args.e2e_epochs, n_columns=nx, n_rows=ny, map_type=mtype,
+                            kernel=S.Kernel.DENSE_BLOCKED, grid=gtype, neighborhood=nb,
+                            compact_support=compact, seed=1)
+        data = S.DenseDataset(Xh)
+        S.train(data, S.TrainConfig(n_epochs=1, n_columns=nx, n_rows=ny, map_type=mtype,
+                                    kernel=S.Kernel.DENSE_BLOCKED, grid=gtype, neighborhood=nb,
+                                    compact_support=compact), options=opts, local_rows=True)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        cb, bmus, u = S.train(data, cfg, options=opts, local_rows=True)
+        torch.cuda.synchronize()
+        barrier()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = float(te.item())
+        e2e = {"value": n * K * args.e2e_epochs / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(count * d * 4 + K * d * 4),
+               "d2h_bytes_per_step": int(K * d * 4 + n * 2 * 4 + K * 4),
+               "step": f"one public train() call: H2D of the rank's rows from pinned memory, "
+                       f"{args.e2e_epochs} epochs, final naive BMU pass, U-matrix, D2H of "
+                       f"codebook + BMU table + U-matrix",
+               "seconds": te}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_rate(args.config, args.ref_rows, 1, 0)
+        cpu.pop("seconds_per_step", None)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "fp16 tensor-core screen (fp32 accumulate) + f64 exact re-rank/update",
+                "data": "synthetic uniform [0,1) fp32 (torch.Generator seed 1001+rank), codebook "
+                        "init default_rng(1)",
+                "config": {"workload": desc, "rows": n, "K": K, "d": d,
+                           "schedule": f"{N_EPOCHS}-epoch linear radius {max(min(nx, ny) / 2, 1)}->1, "
+                                       f"scale 1->0.01; step s = epoch s mod {N_EPOCHS}",
+                           "parallelism": f"dp{world} (rows sharded, 1 fp64 all-reduce + 1 fp32 "
+                                          f"all-gather per epoch)",
+                           "l2": "inputs larger than L2 (X 4 GB + fp16 copy 2 GB per GPU at cfg2)",
+                           "screen": args.screen},
+                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
+                "gpu_launches": int(launches),
+                "phase_ms": phases, "epoch_ms": ms_step,
+                "nkd_per_s": value * d, "window_truncated_rows": trunc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--screen", default="tensor", choices=["tensor", "simt", "exact"])
+    ap.add_argument("--e2e-epochs", type=int, default=10)
+    ap.add_argument("--ref-rows", type=int, default=4096)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -104,7 +104,6 @@ SOMB_API int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const f
  * ties.  Output bmu int32[n], d2min fp64[n] (clamped >= 0), flags int32[n]
  * (bit0 = window truncated).  ws >= somb_bmu_ws(n).  screen_impl: 0 =
  * tcgen05 (sm_100a), 1 = SIMT reference screen (tests). */
-SOMB_API size_t somb_bmu_ws(int64_t n);
 SOMB_API int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xnorm,
                    const double *x2, int64_t n, int32_t d, int32_t dp,
                    const uint16_t *Wh, const float *W, const float *c,
@@ -112,6 +111,20 @@ SOMB_API int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xno
                    float window_coef, int32_t dist_mode, int32_t screen_impl,
                    int32_t *bmu, double *d2min, int32_t *flags, void *ws,
                    void *stream);
+
+/* The two phases of somb_bmu_dense, separately (per-kernel timing):
+ * screen -> ws candidate lists; re-rank -> bmu / d2min. */
+SOMB_API size_t somb_bmu_ws(int64_t n);
+SOMB_API int somb_bmu_screen(const uint16_t *Xh, const float *xnorm, int64_t n,
+                             int32_t dp, const uint16_t *Wh, const float *c,
+                             int32_t kp, const float *scal, float window_coef,
+                             int32_t screen_impl, int32_t *flags, void *ws,
+                             void *stream);
+SOMB_API int somb_bmu_rerank(const float *X, const double *x2, int64_t n,
+                             int32_t d, const float *W, const double *w2,
+                             int32_t K, int32_t dist_mode, int32_t screen_impl,
+                             int32_t *bmu, double *d2min, int32_t *flags,
+                             void *ws, void *stream);
 
 /* qe_sum = sum_i sqrt(d2min_i) in fixed order (kernels.py:407, 427). */
 SOMB_API int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws,
@@ -150,6 +163,9 @@ SOMB_API int somb_hood_update(const double *S, const double *cnt, int32_t d,
  * arithmetic as the fused epilogue of somb_hood_update. */
 SOMB_API int somb_blend(const float *W_old, const double *num, const double *den,
                int32_t K, int32_t d, double scale, float *W_new, void *stream);
+
+/* Number of kernels this library has launched (process lifetime). */
+SOMB_API unsigned long long somb_launch_count(void);
 
 /* ---- U-matrix (umatrix.py:26-45; hex adjacency = extension) ---------- */
 SOMB_API int somb_umatrix(const float *W, int32_t d, const somb_map *map, float *U,

@@ -172,41 +172,58 @@ extern "C" size_t somb_bmu_ws(int64_t n) {
     return align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256) + align_up((size_t)n * sizeof(int), 256);
 }
 
+extern "C" int somb_bmu_screen(const uint16_t *Xh, const float *xnorm, int64_t n, int32_t dp,
+                               const uint16_t *Wh, const float *c, int32_t kp, const float *scal,
+                               float window_coef, int32_t screen_impl, int32_t *flags, void *ws,
+                               void *stream) {
+    SOMB_REQUIRE(dp % 8 == 0 && kp % 256 == 0, SOMB_E_INPUT, "bmu_screen: dp=%d kp=%d", dp, kp);
+    SOMB_REQUIRE(screen_impl >= 0 && screen_impl <= 2, SOMB_E_CONFIG, "bad screen_impl %d", screen_impl);
+    if (n == 0 || screen_impl == 2) return SOMB_OK;
+    cudaStream_t st = as_stream(stream);
+    int *cand = (int *)ws;
+    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
+    if (screen_impl == 0)
+        return launch_screen_tc((const __half *)Xh, n, dp, (const __half *)Wh, kp, c, xnorm, scal,
+                                window_coef, cand, ccount, flags, st);
+    unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
+    screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh, kp, c,
+                                                      xnorm, scal, window_coef, cand, ccount, flags);
+    note_launch();
+    SOMB_LAUNCH_CHECK("screen_simt");
+    return SOMB_OK;
+}
+
+extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int32_t d, const float *W,
+                               const double *w2, int32_t K, int32_t dist_mode, int32_t screen_impl,
+                               int32_t *bmu, double *d2min, int32_t *flags, void *ws, void *stream) {
+    SOMB_REQUIRE(K > 0 && d > 0, SOMB_E_INPUT, "bmu_rerank: bad shape K=%d d=%d", K, d);
+    SOMB_REQUIRE(dist_mode == SOMB_DIST_BLOCKED || dist_mode == SOMB_DIST_NAIVE, SOMB_E_CONFIG,
+                 "bmu_rerank: bad dist_mode %d", dist_mode);
+    if (n == 0) return SOMB_OK;
+    cudaStream_t st = as_stream(stream);
+    int *cand = (int *)ws;
+    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
+    int all = screen_impl == 2, split = screen_impl == 0;
+    if (all) cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
+    const int wpb = 8;
+    rerank_kernel<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
+        X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, split, bmu, d2min);
+    note_launch();
+    SOMB_LAUNCH_CHECK("rerank");
+    return SOMB_OK;
+}
+
 extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xnorm, const double *x2,
                               int64_t n, int32_t d, int32_t dp, const uint16_t *Wh, const float *W,
                               const float *c, const double *w2, int32_t K, int32_t kp,
                               const float *scal, float window_coef, int32_t dist_mode,
                               int32_t screen_impl, int32_t *bmu, double *d2min, int32_t *flags,
                               void *ws, void *stream) {
-    SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && dp % 8 == 0 && kp >= K && kp % 256 == 0, SOMB_E_INPUT,
+    SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && kp >= K, SOMB_E_INPUT,
                  "bmu_dense: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
-    SOMB_REQUIRE(dist_mode == SOMB_DIST_BLOCKED || dist_mode == SOMB_DIST_NAIVE, SOMB_E_CONFIG,
-                 "bmu_dense: bad dist_mode %d", dist_mode);
-    if (n == 0) return SOMB_OK;
-    cudaStream_t st = as_stream(stream);
-    int *cand = (int *)ws;
-    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
-    int all = 0, split = 0;
-    if (screen_impl == 0) {
-        split = 1;
-        int rc = launch_screen_tc((const __half *)Xh, n, dp, (const __half *)Wh, kp, c, xnorm, scal,
-                                  window_coef, cand, ccount, flags, st);
-        if (rc != SOMB_OK) return rc;
-    } else if (screen_impl == 1) {
-        unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
-        screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh,
-                                                          kp, c, xnorm, scal, window_coef, cand, ccount,
-                                                          flags);
-        SOMB_LAUNCH_CHECK("screen_simt");
-    } else {
-        all = 1;
-        cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
-    }
-    const int wpb = 8;
-    rerank_kernel<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
-        X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, split, bmu, d2min);
-    SOMB_LAUNCH_CHECK("rerank");
-    return SOMB_OK;
+    int rc = somb_bmu_screen(Xh, xnorm, n, dp, Wh, c, kp, scal, window_coef, screen_impl, flags, ws, stream);
+    if (rc) return rc;
+    return somb_bmu_rerank(X, x2, n, d, W, w2, K, dist_mode, screen_impl, bmu, d2min, flags, ws, stream);
 }
 
 extern "C" int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws, void *stream) {
@@ -218,7 +235,9 @@ extern "C" int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws
     }
     double *part = (double *)ws;   // >= np doubles (callers pass somb_bmu_ws-sized ws)
     qe_partial<<<np, 256, 0, st>>>(d2min, n, part);
+    note_launch();
     qe_final<<<1, 256, 0, st>>>(part, np, out);
+    note_launch();
     SOMB_LAUNCH_CHECK("qe_sum");
     return SOMB_OK;
 }

@@ -1,6 +1,8 @@
 // Library-level entry points: version, last error, device check.
 #include <stdarg.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace somb {
@@ -11,6 +13,8 @@ void set_error(const char *fmt, ...) {
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
 }
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 __global__ void probe_kernel(int *out) { *out = 1000; }
 }  // namespace somb
 
@@ -31,3 +35,5 @@ extern "C" int somb_device_check(int dev) {
     if (e != cudaSuccess) return somb::cuda_status(e, "kernel image load");
     return SOMB_OK;
 }
+
+extern "C" unsigned long long somb_launch_count(void) { return somb::g_launches.load(); }

@@ -15,6 +15,7 @@
 namespace somb {
 
 void set_error(const char *fmt, ...);
+void note_launch();   // kernel-launch counter (somb_launch_count)
 
 static inline int cuda_status(cudaError_t e, const char *what) {
     if (e == cudaSuccess) return SOMB_OK;

@@ -222,17 +222,22 @@ extern "C" int somb_hood_update(const double *S, const double *cnt, int32_t d, c
     if (den_out) den = den_out;
     hood_table_kernel<<<(tw * m.ny + 255) / 256, 256, 0, st>>>(m, tw, dist_table, hood->neighborhood,
                                                                hood->compact, hood->radius, hood->cutoff, htab);
+    note_launch();
     occ_flags<<<(K + 255) / 256, 256, 0, st>>>(cnt, K, flag);
+    note_launch();
     rc = exclusive_scan(flag, K, pos, st);
     if (rc) return rc;
     occ_scatter<<<(K + 255) / 256, 256, 0, st>>>(flag, pos, K, occ);
+    note_launch();
     const int *nocc = pos + K;
     const int nn = node_end - node_begin;
     if (nn == 0) return SOMB_OK;
     hood_den_kernel<<<(nn + 255) / 256, 256, 0, st>>>(m, tw, htab, cnt, occ, nocc, node_begin, node_end, den);
+    note_launch();
     dim3 g((d + kHN - 1) / kHN, (nn + kHM - 1) / kHM);
     hood_conv_blend<<<g, 256, 0, st>>>(m, tw, htab, S, d, occ, nocc, node_begin, node_end, den, scale,
                                        1.0 - scale, W_old, W_new, num_out);
+    note_launch();
     SOMB_LAUNCH_CHECK("hood_update");
     return SOMB_OK;
 }
@@ -262,6 +267,7 @@ extern "C" int somb_blend(const float *W_old, const double *num, const double *d
     int64_t tot = (int64_t)K * d;
     somb::blend_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, somb::as_stream(stream)>>>(
         W_old, num, den, K, d, scale, 1.0 - scale, W_new);
+    note_launch();
     SOMB_LAUNCH_CHECK("blend");
     return SOMB_OK;
 }

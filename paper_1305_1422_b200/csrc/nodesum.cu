@@ -254,9 +254,12 @@ extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const 
     int *kout = w.kA, *vout = w.vA;
     for (int p = 0; p < passes; ++p) {
         radix_hist<<<ntiles, kSortThreads, 0, st>>>(kin, n, 8 * p, ntiles, w.hist);
+        note_launch();
         exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.hist, 256 * ntiles, w.hsc);
+        note_launch();
         radix_scatter<<<ntiles, kSortThreads, 0, st>>>(kin, vin, n, 8 * p, ntiles, w.hsc, kout, vout,
                                                        p == 0);
+        note_launch();
         kin = kout;
         vin = vout;
         kout = (kout == w.kA) ? w.kB : w.kA;
@@ -266,16 +269,24 @@ extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const 
     if (passes == 0) {   // K == 1: every row in node 0, identity order
         // reuse the scatter kernel as an iota copy with a 0-bit digit
         radix_hist<<<ntiles, kSortThreads, 0, st>>>(bmu, n, 0, ntiles, w.hist);
+        note_launch();
         exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.hist, 256 * ntiles, w.hsc);
+        note_launch();
         radix_scatter<<<ntiles, kSortThreads, 0, st>>>(bmu, nullptr, n, 0, ntiles, w.hsc, w.kA, w.vA, 1);
+        note_launch();
         perm = w.vA;
     }
     // --- bucket offsets and segment plan
     bucket_count<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bmu, n, w.cnt);
+    note_launch();
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.cnt, K, w.off);
+    note_launch();
     seg_plan<<<(K + 255) / 256, 256, 0, st>>>(w.cnt, K, w.nseg, w.mseg, cnt);
+    note_launch();
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.nseg, K, w.segoff);
+    note_launch();
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.mseg, K, w.msegoff);
+    note_launch();
     unsigned maxseg = (unsigned)(K + (n + kSeg - 1) / kSeg);
     if (d <= 128)
         seg_sum<1><<<maxseg, 128, 0, st>>>(X, d, perm, w.off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
@@ -283,7 +294,9 @@ extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const 
         seg_sum<4><<<maxseg, 128, 0, st>>>(X, d, perm, w.off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
     else
         seg_sum<8><<<maxseg, 128, 0, st>>>(X, d, perm, w.off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
+    note_launch();
     seg_fold<<<K, 128, 0, st>>>(w.P, w.msegoff, w.nseg, d, S);
+    note_launch();
     SOMB_LAUNCH_CHECK("node_sums");
     return SOMB_OK;
 }
@@ -291,6 +304,7 @@ extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const 
 namespace somb {
 int exclusive_scan(const int *in, int len, int *out, cudaStream_t st) {
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(in, len, out);
+    note_launch();
     SOMB_LAUNCH_CHECK("exclusive_scan");
     return SOMB_OK;
 }

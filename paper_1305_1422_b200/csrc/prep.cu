@@ -190,7 +190,9 @@ extern "C" int somb_data_stats(const float *X, int64_t n, int32_t d, float *nu, 
     cudaMemsetAsync(absmax, 0, sizeof(float), st);
     dim3 g((d + 127) / 128, kStatChunks);
     data_stats_partial<<<g, 128, 0, st>>>(X, n, d, psum, pmin, pmax);
+    note_launch();
     data_stats_final<<<(d + 127) / 128, 128, 0, st>>>(psum, pmin, pmax, n, d, nu, absmax);
+    note_launch();
     SOMB_LAUNCH_CHECK("somb_data_stats");
     return SOMB_OK;
 }
@@ -203,6 +205,7 @@ extern "C" int somb_data_pack(const float *X, int64_t n, int32_t d, const float 
     int64_t blocks = (n + rows_per_block - 1) / rows_per_block;
     data_pack_kernel<<<(unsigned)blocks, 32 * rows_per_block, 0, as_stream(stream)>>>(
         X, n, d, nu, xexp, (__half *)Xh, dp, xnorm, x2);
+    note_launch();
     SOMB_LAUNCH_CHECK("somb_data_pack");
     return SOMB_OK;
 }
@@ -225,8 +228,11 @@ extern "C" int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const
     float *stats = (float *)p;
     cudaMemsetAsync(stats, 0, 4 * sizeof(float), st);
     cb_colmean<<<(d + 7) / 8, 256, 0, st>>>(W, K, d, nu, mu, mu_nu);
+    note_launch();
     cb_rowstats<<<(K + 7) / 8, 256, 0, st>>>(W, K, d, mu, mu_nu, c, w2, nrm, stats);
+    note_launch();
     cb_pack<<<(kp + 7) / 8, 256, 0, st>>>(W, K, d, mu, xexp, (__half *)Wh, dp, kp, c, stats, scal);
+    note_launch();
     SOMB_LAUNCH_CHECK("somb_codebook_prepare");
     return SOMB_OK;
 }

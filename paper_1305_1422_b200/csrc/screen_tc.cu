@@ -329,6 +329,7 @@ int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int 
     int num_rb = (int)((n + TC_BM - 1) / TC_BM);
     int grid = num_rb < sms ? num_rb : sms;
     screen_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, n, dp, kp, c, xnorm, scal, wcoef, cand, ccount, flags);
+    note_launch();
     SOMB_LAUNCH_CHECK("screen_tc");
     return SOMB_OK;
 }

@@ -66,6 +66,7 @@ extern "C" int somb_umatrix(const float *W, int32_t d, const somb_map *map, floa
     MapDev m{map->n_columns, map->n_rows, map->grid == SOMB_GRID_HEX, map->topology == SOMB_TOROID};
     int K = m.nx * m.ny;
     umatrix_kernel<<<(K + 7) / 8, 256, 0, as_stream(stream)>>>(W, d, m, U);
+    note_launch();
     SOMB_LAUNCH_CHECK("umatrix");
     return SOMB_OK;
 }

@@ -125,7 +125,7 @@ class SomEngine:
     # ------------------------------------------------------------ dataset
     def _upload_dense(self, x):
         if _is_torch(x):
-            xt = x.to(self.dev, dtype=torch.float32).contiguous()
+            xt = x.to(self.dev, dtype=torch.float32, non_blocking=True).contiguous()
         else:
             xh = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
             if not xh.is_pinned():
@@ -168,16 +168,37 @@ class SomEngine:
                   _ptr(self.Wh), self.dp, self.kp, _ptr(self.c), _ptr(self.w2), _ptr(self.scal),
                   _ptr(self.ws), _stream(self.dev))
 
+    # optional per-phase CUDA-event timing (bench.py): name -> [(start, end), ...]
+    timing = None
+
+    def _mark(self, name, start):
+        if self.timing is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(torch.cuda.current_stream(self.dev))
+        if start:
+            self.timing.setdefault(name, []).append([ev, None])
+        else:
+            self.timing[name][-1][1] = ev
+
     def search(self, dist_mode=_lib.DIST_BLOCKED):
         """BMU + d2min for the resident rows against the current codebook."""
+        self._mark("prepare", True)
         self.prepare()
+        self._mark("prepare", False)
         if self.n == 0:
             return
-        _lib.call("somb_bmu_dense", _ptr(self.Xh), _ptr(self.X), _ptr(self.xnorm), _ptr(self.x2),
-                  self.n, self.d, self.dp, _ptr(self.Wh), _ptr(self.W), _ptr(self.c), _ptr(self.w2),
-                  self.K, self.kp, _ptr(self.scal), C.c_float(self.window_coef), dist_mode,
-                  self.screen_impl, _ptr(self.bmu), _ptr(self.d2min), _ptr(self.flags),
-                  _ptr(self.ws), _stream(self.dev))
+        st = _stream(self.dev)
+        self._mark("screen", True)
+        _lib.call("somb_bmu_screen", _ptr(self.Xh), _ptr(self.xnorm), self.n, self.dp, _ptr(self.Wh),
+                  _ptr(self.c), self.kp, _ptr(self.scal), C.c_float(self.window_coef),
+                  self.screen_impl, _ptr(self.flags), _ptr(self.ws), st)
+        self._mark("screen", False)
+        self._mark("rerank", True)
+        _lib.call("somb_bmu_rerank", _ptr(self.X), _ptr(self.x2), self.n, self.d, _ptr(self.W),
+                  _ptr(self.w2), self.K, dist_mode, self.screen_impl, _ptr(self.bmu),
+                  _ptr(self.d2min), _ptr(self.flags), _ptr(self.ws), st)
+        self._mark("rerank", False)
 
     def qe_sum(self):
         _lib.call("somb_qe_sum", _ptr(self.d2min), self.n, _ptr(self.qe), _ptr(self.ws),
@@ -210,10 +231,16 @@ class SomEngine:
     def epoch(self, radius, scale, cutoff, neighborhood=Neighborhood.GAUSSIAN, compact=False):
         """One full training epoch; returns the device qe-sum tensor (no sync)."""
         self.search(_lib.DIST_BLOCKED)
+        self._mark("node_sums", True)
         self.qe_sum()
         self.node_sums()
+        self._mark("node_sums", False)
+        self._mark("allreduce", True)
         self.reduce()
+        self._mark("allreduce", False)
+        self._mark("update", True)
         self.update(radius, scale, cutoff, neighborhood, compact)
+        self._mark("update", False)
         return self.qe
 
     def umatrix(self) -> torch.Tensor:
@@ -221,6 +248,14 @@ class SomEngine:
         _lib.call("somb_umatrix", _ptr(self.W), self.d, C.byref(self.cmap), _ptr(u),
                   _stream(self.dev))
         return u.view(self.ny, self.nx)
+
+    def global_rows(self) -> int:
+        if self.world == 1:
+            return self.n
+        import torch.distributed as dist
+        t = torch.tensor([self.n], dtype=torch.int64, device=self.dev)
+        dist.all_reduce(t, group=self.group)
+        return int(t.item())
 
     def gather_bmus(self) -> np.ndarray:
         """Flat BMU indices of ALL rows (rank order), on every rank."""
