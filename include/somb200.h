@@ -115,11 +115,20 @@ SOMB_API int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xno
 /* The two phases of somb_bmu_dense, separately (per-kernel timing):
  * screen -> ws candidate lists; re-rank -> bmu / d2min. */
 SOMB_API size_t somb_bmu_ws(int64_t n);
+/* prev_bmu (may be NULL): each row's BMU from the previous search; seeds the
+ * screening threshold (does not change the result, only the work). */
 SOMB_API int somb_bmu_screen(const uint16_t *Xh, const float *xnorm, int64_t n,
                              int32_t dp, const uint16_t *Wh, const float *c,
-                             int32_t kp, const float *scal, float window_coef,
+                             int32_t K, int32_t kp, const float *scal,
+                             float window_coef, const int32_t *prev_bmu,
                              int32_t screen_impl, int32_t *flags, void *ws,
                              void *stream);
+/* Calibration: tcgen05 screened values of rows [0, min(n,128)) x kp nodes. */
+SOMB_API int somb_debug_screen_dump(const uint16_t *Xh, const float *xnorm,
+                                    int64_t n, int32_t dp, const uint16_t *Wh,
+                                    const float *c, int32_t kp, const float *scal,
+                                    float window_coef, float *dump, void *ws,
+                                    void *stream);
 SOMB_API int somb_bmu_rerank(const float *X, const double *x2, int64_t n,
                              int32_t d, const float *W, const double *w2,
                              int32_t K, int32_t dist_mode, int32_t screen_impl,

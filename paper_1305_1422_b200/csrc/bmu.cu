@@ -11,7 +11,41 @@ namespace somb {
 
 int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int kp,
                      const float *c, const float *xnorm, const float *scal, float wcoef,
-                     int *cand, int *ccount, int *flags, cudaStream_t st);
+                     const float *thr0, int *cand, int *ccount, int *flags, float *dump,
+                     cudaStream_t st);
+
+// Seed of each row's acceptance threshold from its previous BMU: the screened
+// value of that node (same fp16 operands, fp32 FMA) plus two windows of slack
+// (covers the summation-order difference to the tensor-core value; the
+// window already exceeds twice the screen error).  Any node the screen will
+// keep has r <= r_min + win <= r_prev + win, so seeding never changes the
+// final candidate set -- it only skips transient pushes (cand.cuh).
+__global__ void screen_seed_kernel(const __half *__restrict__ Xh, int64_t n, int dp,
+                                   const __half *__restrict__ Wh, int K, const float *__restrict__ c,
+                                   const float *__restrict__ xnorm, const float *__restrict__ scal,
+                                   float wcoef, const int *__restrict__ prev, float *__restrict__ thr0) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const int j = prev[row];
+    float t = FLT_MAX;
+    if (j >= 0 && j < K) {
+        const __half2 *x = reinterpret_cast<const __half2 *>(Xh + row * (int64_t)dp);
+        const __half2 *w = reinterpret_cast<const __half2 *>(Wh + (int64_t)j * dp);
+        float acc = 0.0f;
+        for (int k = lane; k < dp / 2; k += 32) {
+            float2 a = __half22float2(x[k]), b = __half22float2(w[k]);
+            acc = fmaf(a.x, b.x, acc);
+            acc = fmaf(a.y, b.y, acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        float r = fmaf(acc, scal[0], c[j]);
+        float win = wcoef * xnorm[row] * scal[1];
+        if (r < FLT_MAX) t = r + 2.0f * win;
+    }
+    if (lane == 0) thr0[row] = t;
+}
 
 // --------------------------------------------------------- SIMT screen (v0)
 // Reference implementation of the screen used by the parity tests to check
@@ -23,8 +57,8 @@ constexpr int kSimtK = 64;
 __global__ void __launch_bounds__(kSimtRows)
 screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __half *__restrict__ Wh,
                    int kp, const float *__restrict__ c, const float *__restrict__ xnorm,
-                   const float *__restrict__ scal, float wcoef, int *__restrict__ cand,
-                   int *__restrict__ ccount, int *__restrict__ flags) {
+                   const float *__restrict__ scal, float wcoef, const float *__restrict__ thr0,
+                   int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags) {
     __shared__ float wt[kSimtCols][kSimtK + 1];
     __shared__ float bv[SOMB_CAND_CAP * kSimtRows];
     __shared__ int bi[SOMB_CAND_CAP * kSimtRows];
@@ -35,6 +69,8 @@ screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __hal
     const float nmax = scal[1];
     CandRow<SOMB_CAND_CAP> st;
     cand_init(st, live ? wcoef * xnorm[row] * nmax : 0.0f);
+    if (live && thr0) st.thr = thr0[row];
+    const CandBuf cb{smem_addr(bv + t), smem_addr(bi + t), 4u * kSimtRows};
     const __half *xr = Xh + (live ? row : 0) * (int64_t)dp;
     for (int j0 = 0; j0 < kp; j0 += kSimtCols) {
         float acc[kSimtCols];
@@ -66,13 +102,13 @@ screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __hal
 #pragma unroll 1
             for (int q = 0; q < kSimtCols; ++q) {
                 float r = fmaf(acc[q], m, c[j0 + q]);
-                cand_push<SOMB_CAND_CAP>(st, r, j0 + q, bv + t, bi + t, kSimtRows);
+                cand_push<SOMB_CAND_CAP>(st, r, j0 + q, cb);
             }
         }
     }
     if (live) {
         int *out = cand + row * SOMB_CAND_CAP;
-        ccount[row] = cand_emit<SOMB_CAND_CAP>(st, bv + t, bi + t, kSimtRows, out);
+        ccount[row] = cand_emit<SOMB_CAND_CAP>(st, cb, out);
         flags[row] = st.trunc;
     }
 }
@@ -168,26 +204,34 @@ __global__ void qe_final(const double *__restrict__ part, int np, double *__rest
 
 using namespace somb;
 
+// ws layout: cand [n][CAP] int | ccount [n] int | thr0 [n] float
 extern "C" size_t somb_bmu_ws(int64_t n) {
-    return align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256) + align_up((size_t)n * sizeof(int), 256);
+    return align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256) + 2 * align_up((size_t)n * sizeof(int), 256);
 }
 
 extern "C" int somb_bmu_screen(const uint16_t *Xh, const float *xnorm, int64_t n, int32_t dp,
-                               const uint16_t *Wh, const float *c, int32_t kp, const float *scal,
-                               float window_coef, int32_t screen_impl, int32_t *flags, void *ws,
-                               void *stream) {
+                               const uint16_t *Wh, const float *c, int32_t K, int32_t kp,
+                               const float *scal, float window_coef, const int32_t *prev_bmu,
+                               int32_t screen_impl, int32_t *flags, void *ws, void *stream) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % 256 == 0, SOMB_E_INPUT, "bmu_screen: dp=%d kp=%d", dp, kp);
     SOMB_REQUIRE(screen_impl >= 0 && screen_impl <= 2, SOMB_E_CONFIG, "bad screen_impl %d", screen_impl);
     if (n == 0 || screen_impl == 2) return SOMB_OK;
     cudaStream_t st = as_stream(stream);
     int *cand = (int *)ws;
     int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
+    float *thr0 = nullptr;
+    if (prev_bmu) {
+        thr0 = (float *)((char *)ccount + align_up((size_t)n * sizeof(int), 256));
+        screen_seed_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh,
+                                                                     K, c, xnorm, scal, window_coef, prev_bmu, thr0);
+        note_launch();
+    }
     if (screen_impl == 0)
         return launch_screen_tc((const __half *)Xh, n, dp, (const __half *)Wh, kp, c, xnorm, scal,
-                                window_coef, cand, ccount, flags, st);
+                                window_coef, thr0, cand, ccount, flags, nullptr, st);
     unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
     screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh, kp, c,
-                                                      xnorm, scal, window_coef, cand, ccount, flags);
+                                                      xnorm, scal, window_coef, thr0, cand, ccount, flags);
     note_launch();
     SOMB_LAUNCH_CHECK("screen_simt");
     return SOMB_OK;
@@ -221,7 +265,8 @@ extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *x
                               void *ws, void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && kp >= K, SOMB_E_INPUT,
                  "bmu_dense: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
-    int rc = somb_bmu_screen(Xh, xnorm, n, dp, Wh, c, kp, scal, window_coef, screen_impl, flags, ws, stream);
+    int rc = somb_bmu_screen(Xh, xnorm, n, dp, Wh, c, K, kp, scal, window_coef, nullptr, screen_impl, flags,
+                             ws, stream);
     if (rc) return rc;
     return somb_bmu_rerank(X, x2, n, d, W, w2, K, dist_mode, screen_impl, bmu, d2min, flags, ws, stream);
 }
@@ -240,4 +285,18 @@ extern "C" int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws
     note_launch();
     SOMB_LAUNCH_CHECK("qe_sum");
     return SOMB_OK;
+}
+
+// Debug/calibration: screened values r_j of rows [0, min(n, 128)) for all kp
+// nodes from the tcgen05 kernel (dump [128][kp] f32); candidates are
+// computed as usual.  Used to measure the real screen error.
+extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const float *xnorm, int64_t n, int32_t dp,
+                                      const uint16_t *Wh, const float *c, int32_t kp, const float *scal,
+                                      float window_coef, float *dump, void *ws, void *stream) {
+    int64_t m = n < 128 ? n : 128;
+    int *cand = (int *)ws;
+    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
+    int *flags = (int *)((char *)ccount + align_up((size_t)n * sizeof(int), 256));
+    return launch_screen_tc((const __half *)Xh, m, dp, (const __half *)Wh, kp, c, xnorm, scal, window_coef,
+                            nullptr, cand, ccount, flags, dump, as_stream(stream));
 }

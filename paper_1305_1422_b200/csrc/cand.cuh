@@ -12,12 +12,42 @@
 // lowest indices among exact screened ties.  Exact fp64 re-ranking of this
 // set (rerank kernel) picks the BMU with first-minimum ties
 // (kernels.py:27-28, 203).
+//
+// The acceptance threshold `thr` may additionally be lowered by any value
+// the sweep is guaranteed to meet (cand_bound): a chunk's minimum before its
+// elements are pushed, or a seed from the row's previous BMU.  That only
+// removes transient entries that the final filter would drop anyway.
+//
+// Buffers live in shared memory and are addressed with 32-bit shared-window
+// addresses (slot e of a thread at base + e * stride bytes).
 #pragma once
 #include <float.h>
 
 #include "common.cuh"
 
 namespace somb {
+
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts_s32(uint32_t a, int v) {
+    asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+struct CandBuf {
+    uint32_t v, i;      // shared addresses of this thread's slot 0 (values, indices)
+    uint32_t stride;    // bytes between slots
+};
 
 template <int CAP>
 struct CandRow {
@@ -38,18 +68,21 @@ __device__ __forceinline__ void cand_init(CandRow<CAP> &s, float win) {
     s.trunc = 0;
 }
 
-// Slot e of the thread's buffer lives at [e * stride] (stride = #threads
-// sharing the buffer array: conflict-free when lanes touch the same slot).
 template <int CAP>
-__device__ __noinline__ void cand_make_room(CandRow<CAP> &s, float *bv, int *bi, int stride) {
+__device__ __forceinline__ void cand_bound(CandRow<CAP> &s, float r_seen) {
+    s.thr = fminf(s.thr, r_seen + s.win);
+}
+
+template <int CAP>
+__device__ __noinline__ void cand_make_room(CandRow<CAP> &s, CandBuf b) {
     const float lim = s.rmin + s.win;
     int m = 0;
     for (int e = 0; e < s.cnt; ++e) {
-        float v = bv[e * stride];
-        int ix = bi[e * stride];
+        float v = lds_f32(b.v + e * b.stride);
+        int ix = lds_s32(b.i + e * b.stride);
         if (v <= lim) {
-            bv[m * stride] = v;
-            bi[m * stride] = ix;
+            sts_f32(b.v + m * b.stride, v);
+            sts_s32(b.i + m * b.stride, ix);
             ++m;
         }
     }
@@ -61,12 +94,12 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, float *bv, int *bi,
     float capv = -INFINITY;
     unsigned long long keep = 0ull;
     for (int e = 0; e < CAP; ++e) {
-        float v = bv[e * stride];
-        int ix = bi[e * stride];
+        float v = lds_f32(b.v + e * b.stride);
+        int ix = lds_s32(b.i + e * b.stride);
         int rank = 0;
         for (int f = 0; f < CAP; ++f) {
-            float u = bv[f * stride];
-            int iu = bi[f * stride];
+            float u = lds_f32(b.v + f * b.stride);
+            int iu = lds_s32(b.i + f * b.stride);
             rank += (u < v) || (u == v && iu < ix);
         }
         if (rank < H) {
@@ -77,29 +110,28 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, float *bv, int *bi,
     m = 0;
     for (int e = 0; e < CAP; ++e) {
         if (keep >> e & 1ull) {
-            bv[m * stride] = bv[e * stride];
-            bi[m * stride] = bi[e * stride];
+            sts_f32(b.v + m * b.stride, lds_f32(b.v + e * b.stride));
+            sts_s32(b.i + m * b.stride, lds_s32(b.i + e * b.stride));
             ++m;
         }
     }
     s.cnt = m;
     s.trunc = 1;
     s.capbelow = fminf(s.capbelow, nextafterf(capv, -INFINITY));
-    s.thr = fminf(s.rmin + s.win, s.capbelow);
+    s.thr = fminf(s.thr, s.capbelow);
 }
 
 template <int CAP>
-__device__ __forceinline__ void cand_push(CandRow<CAP> &s, float r, int j, float *bv, int *bi,
-                                          int stride) {
+__device__ __forceinline__ void cand_push(CandRow<CAP> &s, float r, int j, CandBuf b) {
     if (r <= s.thr) {
         if (r < s.rmin) {
             s.rmin = r;
-            s.thr = fminf(r + s.win, s.capbelow);
+            s.thr = fminf(s.thr, r + s.win);
         }
-        if (s.cnt == CAP) cand_make_room<CAP>(s, bv, bi, stride);
+        if (s.cnt == CAP) cand_make_room<CAP>(s, b);
         if (r <= s.thr) {
-            bv[s.cnt * stride] = r;
-            bi[s.cnt * stride] = j;
+            sts_f32(b.v + s.cnt * b.stride, r);
+            sts_s32(b.i + s.cnt * b.stride, j);
             ++s.cnt;
         }
     }
@@ -107,12 +139,11 @@ __device__ __forceinline__ void cand_push(CandRow<CAP> &s, float r, int j, float
 
 // Final filter: write { held j : r_j <= rmin + win } in index order.
 template <int CAP>
-__device__ __forceinline__ int cand_emit(const CandRow<CAP> &s, const float *bv, const int *bi,
-                                         int stride, int *out) {
+__device__ __forceinline__ int cand_emit(const CandRow<CAP> &s, CandBuf b, int *out) {
     const float lim = s.rmin + s.win;
     int m = 0;
     for (int e = 0; e < s.cnt; ++e)
-        if (bv[e * stride] <= lim) out[m++] = bi[e * stride];
+        if (lds_f32(b.v + e * b.stride) <= lim) out[m++] = lds_s32(b.i + e * b.stride);
     return m;
 }
 

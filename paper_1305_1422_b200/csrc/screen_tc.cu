@@ -121,8 +121,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 __global__ void __launch_bounds__(TC_THREADS, 1)
 screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                  int64_t n, int dp, int kp, const float *__restrict__ c, const float *__restrict__ xnorm,
-                 const float *__restrict__ scal, float wcoef, int *__restrict__ cand,
-                 int *__restrict__ ccount, int *__restrict__ flags) {
+                 const float *__restrict__ scal, float wcoef, const float *__restrict__ thr0,
+                 int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags,
+                 float *__restrict__ dump) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = smem;                                     // [stage][16 KB]
@@ -211,15 +212,16 @@ screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
         }
     } else {
         // ---------------------------------------------------------- epilogue
+        // Warp group `half` takes the 32-column chunks ch = half, half+2, ...
+        // of each 256-node tile (interleaved so that a run of consecutive
+        // nodes -- neighbours on the map -- spreads over both groups).
         const int ew = warp - 2;               // 0..7
         const int quad = warp & 3;             // TMEM lane quadrant this warp may access
-        const int half = ew >> 2;              // column half of each 256-node tile
+        const int half = ew >> 2;
         const int et = ew * 32 + lane;         // buffer slot owner id
         const float m = scal[0];
         const float nmax = scal[1];
-        float *bv = cbv + et;
-        int *bi = cbi + et;
-        constexpr int stride = TC_EPI_WARPS * 32;
+        const CandBuf cb{smem_u32(cbv + et), smem_u32(cbi + et), 4u * TC_EPI_WARPS * 32};
         int acc = 0;
         uint32_t aphase = 0;
         for (int rb = blockIdx.x; rb < num_rb; rb += gridDim.x) {
@@ -227,16 +229,17 @@ screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             const bool live = row < n;
             CandRow<TC_HALF_CAP> st;
             cand_init(st, live ? wcoef * xnorm[row] * nmax : 0.0f);
+            if (live && thr0) st.thr = thr0[row];
+            const bool dumping = dump != nullptr && live;
             for (int nt = 0; nt < NT; ++nt) {
                 mbar_wait(tfull0 + 8 * acc, aphase);
                 tc_fence_after();
-                const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + half * 128);
-                const int j0 = nt * TC_BN + half * 128;
+                const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN);
 #pragma unroll 1
-                for (int ch = 0; ch < 4; ++ch) {
+                for (int ch = half; ch < TC_BN / 32; ch += 2) {
                     float v[32];
                     tmem_ld32(tbase + ch * 32, v);
-                    const int jc = j0 + ch * 32;
+                    const int jc = nt * TC_BN + ch * 32;
                     const float4 *cp = reinterpret_cast<const float4 *>(c + jc);
                     float lo = INFINITY;
 #pragma unroll
@@ -248,10 +251,15 @@ screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                         v[4 * q + 3] = fmaf(v[4 * q + 3], m, cc.w);
                         lo = fminf(lo, fminf(fminf(v[4 * q], v[4 * q + 1]), fminf(v[4 * q + 2], v[4 * q + 3])));
                     }
+                    if (dumping) {
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) dump[row * kp + jc + q] = v[q];
+                    }
                     if (live && lo <= st.thr) {
+                        cand_bound(st, lo);   // the chunk minimum is about to be pushed
 #pragma unroll
                         for (int q = 0; q < 32; ++q)
-                            if (v[q] <= st.thr) cand_push<TC_HALF_CAP>(st, v[q], jc + q, bv, bi, stride);
+                            if (v[q] <= st.thr) cand_push<TC_HALF_CAP>(st, v[q], jc + q, cb);
                     }
                 }
                 tc_fence_before();
@@ -260,7 +268,7 @@ screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             }
             if (live) {
                 int *out = cand + row * SOMB_CAND_CAP + half * TC_HALF_CAP;
-                int cnt = cand_emit<TC_HALF_CAP>(st, bv, bi, stride, out);
+                int cnt = cand_emit<TC_HALF_CAP>(st, cb, out);
                 // two halves write disjoint bytes of ccount / flags
                 reinterpret_cast<uint8_t *>(ccount + row)[half] = (uint8_t)cnt;
                 reinterpret_cast<uint8_t *>(flags + row)[half] = (uint8_t)st.trunc;
@@ -307,8 +315,8 @@ static int make_map(CUtensorMap *map, const void *base, uint64_t inner, uint64_t
 }
 
 int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int kp, const float *c,
-                     const float *xnorm, const float *scal, float wcoef, int *cand, int *ccount, int *flags,
-                     cudaStream_t st) {
+                     const float *xnorm, const float *scal, float wcoef, const float *thr0, int *cand,
+                     int *ccount, int *flags, float *dump, cudaStream_t st) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % TC_BN == 0, SOMB_E_INPUT, "screen_tc: dp %% 8 and kp %% 256 required");
     CUtensorMap mx, mw;
     int rc = make_map(&mx, Xh, (uint64_t)dp, (uint64_t)n, TC_BM);
@@ -328,7 +336,8 @@ int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int 
     cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
     int num_rb = (int)((n + TC_BM - 1) / TC_BM);
     int grid = num_rb < sms ? num_rb : sms;
-    screen_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, n, dp, kp, c, xnorm, scal, wcoef, cand, ccount, flags);
+    screen_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
+                                                        flags, dump);
     note_launch();
     SOMB_LAUNCH_CHECK("screen_tc");
     return SOMB_OK;

@@ -24,7 +24,7 @@ from . import _lib, errors
 from .datasets import DenseDataset, SparseDataset, _is_torch
 from .grid import GridType, MapType, Neighborhood, distance_table
 
-_DEF_WINDOW_KAPPA = 24.0   # screening window, in fp16-rounding units
+_DEF_WINDOW_KAPPA = 16.0   # screening window = kappa * u16 * |x-nu| * max|delta| / sqrt(D); measured max screen error <= 6.1 units (tools/calib_screen.py), so the window covers 2x that with 30% margin
 _U16 = 2.0 ** -11
 
 
@@ -33,6 +33,7 @@ class EngineOptions:
     screen: str = "tensor"            # "tensor" (tcgen05), "simt" (reference screen), "exact"
     window_kappa: float = _DEF_WINDOW_KAPPA
     hypot_table: bool = True          # numpy-hypot distances for rect grids (bit parity)
+    seed_prev: bool = True            # seed the screen threshold from the previous BMUs
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -121,6 +122,7 @@ class SomEngine:
         self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)
         self.window_coef = float(self.opt.window_kappa * _U16 / math.sqrt(d))
         self.screen_impl = {"tensor": 0, "simt": 1, "exact": 2}[self.opt.screen]
+        self.has_prev = False
 
     # ------------------------------------------------------------ dataset
     def _upload_dense(self, x):
@@ -190,15 +192,35 @@ class SomEngine:
             return
         st = _stream(self.dev)
         self._mark("screen", True)
+        prev = self.bmu if (self.has_prev and self.opt.seed_prev) else None
         _lib.call("somb_bmu_screen", _ptr(self.Xh), _ptr(self.xnorm), self.n, self.dp, _ptr(self.Wh),
-                  _ptr(self.c), self.kp, _ptr(self.scal), C.c_float(self.window_coef),
-                  self.screen_impl, _ptr(self.flags), _ptr(self.ws), st)
+                  _ptr(self.c), self.K, self.kp, _ptr(self.scal), C.c_float(self.window_coef),
+                  _ptr(prev), self.screen_impl, _ptr(self.flags), _ptr(self.ws), st)
         self._mark("screen", False)
         self._mark("rerank", True)
         _lib.call("somb_bmu_rerank", _ptr(self.X), _ptr(self.x2), self.n, self.d, _ptr(self.W),
                   _ptr(self.w2), self.K, dist_mode, self.screen_impl, _ptr(self.bmu),
                   _ptr(self.d2min), _ptr(self.flags), _ptr(self.ws), st)
         self._mark("rerank", False)
+        self.has_prev = True
+
+    def debug_screen_values(self) -> torch.Tensor:
+        """tcgen05 screened values r~ of rows [0, 128) x all nodes (calibration)."""
+        self.prepare()
+        m = min(self.n, 128)
+        dump = torch.full((m, self.kp), float("nan"), dtype=torch.float32, device=self.dev)
+        _lib.call("somb_debug_screen_dump", _ptr(self.Xh), _ptr(self.xnorm), self.n, self.dp,
+                  _ptr(self.Wh), _ptr(self.c), self.kp, _ptr(self.scal), C.c_float(self.window_coef),
+                  _ptr(dump), _ptr(self.ws), _stream(self.dev))
+        return dump[:, : self.K]
+
+    def candidate_counts(self) -> torch.Tensor:
+        """Per-row candidate counts of the last screen (tcgen05 two-half encoding)."""
+        off = ((self.n * _lib.CAND_CAP * 4 + 255) // 256) * 256
+        cc = self.ws[off: off + 4 * self.n].view(torch.int32)
+        if self.screen_impl == 0:
+            return (cc & 255) + ((cc >> 8) & 255)
+        return cc
 
     def qe_sum(self):
         _lib.call("somb_qe_sum", _ptr(self.d2min), self.n, _ptr(self.qe), _ptr(self.ws),
