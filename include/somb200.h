@@ -60,7 +60,13 @@ typedef struct somb_hood {
     int32_t compact;            /* 1: h = 0 beyond radius (extension)    */
     double radius;              /* epoch radius (train.py:209-217)       */
     double cutoff;              /* h < cutoff -> 0 (kernels.py:146-147)  */
+    int32_t method;             /* SOMB_CONV_*: 0 auto, 1 direct, 2 spectral */
+    int32_t reserved;
 } somb_hood;
+
+#define SOMB_CONV_AUTO 0
+#define SOMB_CONV_DIRECT 1      /* fp64 sum over occupied nodes, O(K^2 D)   */
+#define SOMB_CONV_SPECTRAL 2    /* fp64 DFT along x + per-frequency GEMM    */
 
 /* Screening parameters of the tensor-core BMU search. */
 #define SOMB_CAND_CAP 32        /* candidates kept per row               */
@@ -160,7 +166,7 @@ SOMB_API int somb_node_sums_dense(const float *X, int64_t n, int32_t d,
  * (rect: n_rows x n_columns) -- the host passes numpy's hypot table so d is
  * bit-identical to kernels.py:112; NULL computes sqrt(dx^2 + dy^2).
  * ws >= somb_hood_ws(map, K). */
-SOMB_API size_t somb_hood_ws(const somb_map *map, int32_t K);
+SOMB_API size_t somb_hood_ws(const somb_map *map, int32_t K, int32_t d);
 SOMB_API int somb_hood_update(const double *S, const double *cnt, int32_t d,
                      const somb_map *map, const somb_hood *hood, double scale,
                      const double *dist_table,

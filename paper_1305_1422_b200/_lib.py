@@ -30,7 +30,11 @@ class SombMap(C.Structure):
 
 class SombHood(C.Structure):
     _fields_ = [("neighborhood", C.c_int32), ("compact", C.c_int32),
-                ("radius", C.c_double), ("cutoff", C.c_double)]
+                ("radius", C.c_double), ("cutoff", C.c_double),
+                ("method", C.c_int32), ("reserved", C.c_int32)]
+
+
+CONV_AUTO, CONV_DIRECT, CONV_SPECTRAL = 0, 1, 2
 
 
 P = C.c_void_p
@@ -56,7 +60,7 @@ SIGNATURES = {
     "somb_launch_count": (C.c_ulonglong, []),
     "somb_node_sums_ws": (SZ, [I64, I32, I32]),
     "somb_node_sums_dense": (C.c_int, [P, I64, I32, P, I32, P, P, P, P]),
-    "somb_hood_ws": (SZ, [C.POINTER(SombMap), I32]),
+    "somb_hood_ws": (SZ, [C.POINTER(SombMap), I32, I32]),
     "somb_hood_update": (C.c_int, [P, P, I32, C.POINTER(SombMap), C.POINTER(SombHood), F64, P,
                                    P, I32, I32, P, P, P, P, P]),
     "somb_blend": (C.c_int, [P, P, P, I32, I32, F64, P, P]),

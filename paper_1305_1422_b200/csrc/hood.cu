@@ -177,6 +177,9 @@ hood_conv_blend(MapDev m, int tw, const double *__restrict__ htab, const double 
 }
 
 int exclusive_scan(const int *in, int len, int *out, cudaStream_t st);
+size_t spec_ws_bytes(const somb_map *m, int d);
+int spec_update(const somb_map *m, const double *htab, const double *S, int d, const double *den, double scale,
+                const float *Wold, int j0, int j1, float *Wnew, double *num_out, void *ws, cudaStream_t st);
 
 }  // namespace somb
 
@@ -184,9 +187,19 @@ using namespace somb;
 
 static int table_width(const somb_map *m) { return m->grid == SOMB_GRID_HEX ? 2 * m->n_columns : m->n_columns; }
 
-extern "C" size_t somb_hood_ws(const somb_map *map, int32_t K) {
+static size_t direct_ws(const somb_map *map, int32_t K) {
     return 3 * align_up((size_t)(K + 1) * sizeof(int), 256) + align_up((size_t)K * sizeof(double), 256) +
            align_up((size_t)table_width(map) * map->n_rows * sizeof(double), 256) + 256;
+}
+
+extern "C" size_t somb_hood_ws(const somb_map *map, int32_t K, int32_t d) {
+    return direct_ws(map, K) + spec_ws_bytes(map, d);
+}
+
+static bool use_spectral(const somb_map *m, const somb_hood *h) {
+    if (h->method == SOMB_CONV_DIRECT) return false;
+    if (h->method == SOMB_CONV_SPECTRAL) return true;
+    return (int64_t)m->n_columns * m->n_rows >= 2048;
 }
 
 static int check_map(const somb_map *m) {
@@ -234,6 +247,10 @@ extern "C" int somb_hood_update(const double *S, const double *cnt, int32_t d, c
     if (nn == 0) return SOMB_OK;
     hood_den_kernel<<<(nn + 255) / 256, 256, 0, st>>>(m, tw, htab, cnt, occ, nocc, node_begin, node_end, den);
     note_launch();
+    if (use_spectral(map, hood)) {
+        char *sws = (char *)ws + direct_ws(map, K);
+        return spec_update(map, htab, S, d, den, scale, W_old, node_begin, node_end, W_new, num_out, sws, st);
+    }
     dim3 g((d + kHN - 1) / kHN, (nn + kHM - 1) / kHM);
     hood_conv_blend<<<g, 256, 0, st>>>(m, tw, htab, S, d, occ, nocc, node_begin, node_end, den, scale,
                                        1.0 - scale, W_old, W_new, num_out);

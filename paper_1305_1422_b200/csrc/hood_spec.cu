@@ -1,0 +1,306 @@
+// Spectral neighbourhood convolution (fp64): num = H S without the O(K^2 D)
+// direct sum.
+//
+// h(b, j) depends on the row offset dy (and, on the hex lattice, on the half
+// column shift between odd and even rows) and on the column offset t =
+// c_j - c_b only.  For every pair of map rows (y_out, y_in) the x-direction
+// is therefore a 1-D convolution with a kernel k_{key}[t], key = (dy,
+// shift).  A length-L DFT along x diagonalises it:
+//   S^[y][f]     = sum_c S[y][c] w^{-fc}                      (fwd, real->complex)
+//   N^[y_o][f]   = sum_{y_i} k^_{key(y_o,y_i)}[f] S^[y_i][f]   (complex GEMM per f)
+//   num[y_o][c]  = 1/L sum_f wt_f Re(N^[y_o][f] w^{fc})       (inv, fused blend)
+// with L = nx on toroids (circular = the reference's min-wrap, kernels.py:
+// 109-111) and L = 2 nx on planar maps (zero padding => linear convolution,
+// no wrap).  Only the F = L/2 + 1 non-redundant frequencies of the real
+// input are carried.  Every step runs in fp64 through one tiled DFMA GEMM
+// template with functional operand loaders; the influence values are the same
+// htab entries the direct path uses (hood.cu), and den (with its exact zero
+// pattern for the den > 0 blend mask) still comes from the direct fp64 sum.
+// Cost ~ F ny^2 D + 4 K F D complex MACs instead of K^2 D.
+#include "common.cuh"
+
+namespace somb {
+
+struct SpecGeom {
+    int nx, ny, L, F, hex, toroid, tw;
+};
+
+// ------------------------------------------------------- generic DFMA GEMM
+// C(b)[M x N] = A(b)[M x K] * B(b)[K x N]; loaders return A(b, m, k) /
+// B(b, k, n) (0 outside), the epilogue consumes (b, m, n, value).
+constexpr int GM = 64, GN = 64, GK = 16;
+
+template <class AL, class BL, class EP>
+__global__ void __launch_bounds__(256) dgemm_fn(int M, int N, int Kd, AL al, BL bl, EP ep) {
+    __shared__ double sa[GK][GM + 1];
+    __shared__ double sb[GK][GN];
+    const int t = threadIdx.x, tx = t % 16, ty = t / 16;
+    const int b = blockIdx.z;
+    const int m0 = blockIdx.y * GM, n0 = blockIdx.x * GN;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < Kd; k0 += GK) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            int e = t + 256 * q;              // 0..1023
+            int kk = e / GM, mm = e % GM;     // A tile: 16 x 64 (k-major in smem)
+            int m = m0 + mm, k = k0 + kk;
+            sa[kk][mm] = (m < M && k < Kd) ? al(b, m, k) : 0.0;
+            int kb = e / GN, nn = e % GN;     // B tile: 16 x 64
+            int n = n0 + nn, k2 = k0 + kb;
+            sb[kb][nn] = (n < N && k2 < Kd) ? bl(b, k2, n) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < GK; ++kk) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = sa[kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = sb[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(av[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int m = m0 + ty + 16 * i;
+        if (m >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int n = n0 + tx + 16 * j;
+            if (n < N) ep(b, m, n, acc[i][j]);
+        }
+    }
+}
+
+template <class AL, class BL, class EP>
+static void dgemm_launch(int batch, int M, int N, int Kd, AL al, BL bl, EP ep, cudaStream_t st) {
+    dim3 g((N + GN - 1) / GN, (M + GM - 1) / GM, batch);
+    dgemm_fn<<<g, 256, 0, st>>>(M, N, Kd, al, bl, ep);
+    note_launch();
+}
+
+// ------------------------------------------------------------------ tables
+// twiddles: cs[q] = cos(2 pi q / L), sn[q] = sin(2 pi q / L), q in [0, L)
+__global__ void spec_twiddle(int L, double *cs, double *sn) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= L) return;
+    double s, c;
+    sincospi(2.0 * (double)q / (double)L, &s, &c);
+    cs[q] = c;
+    sn[q] = s;
+}
+
+__device__ __forceinline__ int spec_nkeys_dev(const SpecGeom &g) {
+    int ndy = g.toroid ? g.ny / 2 + 1 : g.ny;
+    return g.hex ? 3 * ndy : ndy;
+}
+
+// key of a row pair: dy (wrapped on toroids) and, on hex, the half-column
+// shift sh = (y_out & 1) - (y_in & 1) in {-1, 0, 1}
+__device__ __forceinline__ int spec_key(const SpecGeom &g, int yo, int yi) {
+    int dy = abs(yo - yi);
+    if (g.toroid) dy = min(dy, g.ny - dy);
+    if (!g.hex) return dy;
+    int sh = (yo & 1) - (yi & 1);
+    return dy * 3 + (sh + 1);
+}
+
+// k^[key][f] = sum_t k[t] w^{-f t}; ktab layout [key][2][F] (re, im)
+__global__ void spec_kernel_table(SpecGeom g, const double *__restrict__ htab, const double *__restrict__ cs,
+                                  const double *__restrict__ sn, double *__restrict__ ktab) {
+    extern __shared__ double kt[];   // L values of k[t]
+    const int key = blockIdx.x;
+    const int dy = g.hex ? key / 3 : key;
+    const int sh = g.hex ? key % 3 - 1 : 0;
+    for (int t = threadIdx.x; t < g.L; t += blockDim.x) {
+        // signed column offset t_s = c_out - c_in
+        int ts = t;
+        double v = 0.0;
+        bool valid = true;
+        if (!g.toroid) {
+            ts = t < g.nx ? t : t - g.L;              // L = 2 nx
+            if (ts <= -g.nx || ts >= g.nx) valid = false;
+        }
+        if (valid) {
+            int idx;
+            if (!g.hex) {
+                int dx = abs(ts);
+                if (g.toroid) dx = min(dx % g.nx, g.nx - dx % g.nx);
+                idx = dy * g.tw + dx;
+            } else {
+                int dx2 = abs(2 * ts + sh);
+                if (g.toroid) {
+                    dx2 %= 2 * g.nx;
+                    dx2 = min(dx2, 2 * g.nx - dx2);
+                }
+                idx = dy * g.tw + dx2;
+            }
+            v = htab[idx];
+        }
+        kt[t] = v;
+    }
+    __syncthreads();
+    for (int f = threadIdx.x; f < g.F; f += blockDim.x) {
+        double re = 0.0, im = 0.0;
+        int q = 0;                                     // (f * t) mod L, incremental
+        for (int t = 0; t < g.L; ++t) {
+            double v = kt[t];
+            re = __fma_rn(v, cs[q], re);
+            im = __fma_rn(-v, sn[q], im);
+            q += f;
+            if (q >= g.L) q -= g.L;
+        }
+        ktab[((int64_t)key * 2 + 0) * g.F + f] = re;
+        ktab[((int64_t)key * 2 + 1) * g.F + f] = im;
+    }
+}
+
+// ----------------------------------------------------------- GEMM operands
+// fwd: A = Phi [2F x nx] (cos rows then -sin rows), B = S_y [nx x D]
+struct FwdA {
+    SpecGeom g; const double *cs, *sn;
+    __device__ double operator()(int, int r, int c) const {
+        int f = r < g.F ? r : r - g.F;
+        int q = (int)(((int64_t)f * c) % g.L);
+        return r < g.F ? cs[q] : -sn[q];
+    }
+};
+struct FwdB {
+    SpecGeom g; const double *S; int D;
+    __device__ double operator()(int y, int c, int d) const {
+        return c < g.nx ? S[((int64_t)y * g.nx + c) * D + d] : 0.0;
+    }
+};
+// Shat layout [plane][f][y][d]
+struct FwdEp {
+    SpecGeom g; double *Sh; int D;
+    __device__ void operator()(int y, int r, int d, double v) const {
+        int plane = r >= g.F, f = r - plane * g.F;
+        Sh[(((int64_t)plane * g.F + f) * g.ny + y) * D + d] = v;
+    }
+};
+// mid: per f, [Nr; Ni] = [[Kr, -Ki], [Ki, Kr]] [Sr; Si], rows y_out in [y0, y0+nyo)
+struct MidA {
+    SpecGeom g; const double *ktab; int y0, nyo;
+    __device__ double operator()(int f, int r, int k) const {
+        int pr = r >= nyo, pk = k >= g.ny;
+        int yo = y0 + r - pr * nyo, yi = k - pk * g.ny;
+        int key = spec_key(g, yo, yi);
+        double kr = ktab[((int64_t)key * 2 + 0) * g.F + f];
+        double ki = ktab[((int64_t)key * 2 + 1) * g.F + f];
+        if (!pr) return pk ? -ki : kr;
+        return pk ? kr : ki;
+    }
+};
+struct MidB {
+    SpecGeom g; const double *Sh; int D;
+    __device__ double operator()(int f, int k, int d) const {
+        int pk = k >= g.ny, yi = k - pk * g.ny;
+        return Sh[(((int64_t)pk * g.F + f) * g.ny + yi) * D + d];
+    }
+};
+// Nhat layout [plane][f][y_local][d]
+struct MidEp {
+    SpecGeom g; double *Nh; int nyo, D;
+    __device__ void operator()(int f, int r, int d, double v) const {
+        int pr = r >= nyo, yl = r - pr * nyo;
+        Nh[(((int64_t)pr * g.F + f) * nyo + yl) * D + d] = v;
+    }
+};
+// inv: num_y [nx x D] = Psi [nx x 2F] * [Nr_y; Ni_y]
+struct InvA {
+    SpecGeom g; const double *cs, *sn;
+    __device__ double operator()(int, int c, int q2) const {
+        int plane = q2 >= g.F, f = q2 - plane * g.F;
+        double w = (f == 0 || 2 * f == g.L) ? 1.0 : 2.0;
+        int q = (int)(((int64_t)f * c) % g.L);
+        double v = plane ? -sn[q] : cs[q];
+        return w * v / (double)g.L;
+    }
+};
+struct InvB {
+    SpecGeom g; const double *Nh; int nyo, D;
+    __device__ double operator()(int yl, int q2, int d) const {
+        int plane = q2 >= g.F, f = q2 - plane * g.F;
+        return Nh[(((int64_t)plane * g.F + f) * nyo + yl) * D + d];
+    }
+};
+struct InvEp {
+    SpecGeom g; int y0, j0, j1, D;
+    const double *den; double alpha, oma;
+    const float *Wold; float *Wnew; double *num_out;
+    __device__ void operator()(int yl, int c, int d, double num) const {
+        if (c >= g.nx) return;
+        int j = (y0 + yl) * g.nx + c;
+        if (j < j0 || j >= j1) return;
+        int64_t o = (int64_t)j * D + d;
+        if (num_out) num_out[o] = num;
+        float w = Wold[o];
+        double dj = den[j];
+        if (dj > 0.0) {
+            double upd = __ddiv_rn(num, dj);
+            w = __double2float_rn(__dadd_rn(__dmul_rn(oma, (double)w), __dmul_rn(alpha, upd)));
+        }
+        Wnew[o] = w;
+    }
+};
+
+static SpecGeom spec_geom(const somb_map *m) {
+    SpecGeom g;
+    g.nx = m->n_columns;
+    g.ny = m->n_rows;
+    g.hex = m->grid == SOMB_GRID_HEX;
+    g.toroid = m->topology == SOMB_TOROID;
+    g.L = g.toroid ? g.nx : 2 * g.nx;
+    g.F = g.L / 2 + 1;
+    g.tw = g.hex ? 2 * g.nx : g.nx;
+    return g;
+}
+
+static int spec_nkeys(const SpecGeom &g) {
+    int ndy = g.toroid ? g.ny / 2 + 1 : g.ny;
+    return g.hex ? 3 * ndy : ndy;
+}
+
+size_t spec_ws_bytes(const somb_map *m, int d) {
+    SpecGeom g = spec_geom(m);
+    size_t b = 2 * align_up((size_t)g.L * 8, 256);
+    b += align_up((size_t)spec_nkeys(g) * 2 * g.F * 8, 256);
+    b += align_up((size_t)2 * g.F * g.ny * d * 8, 256);      // Shat
+    b += align_up((size_t)2 * g.F * g.ny * d * 8, 256);      // Nhat (worst case: all rows)
+    return b;
+}
+
+int spec_update(const somb_map *m, const double *htab, const double *S, int d, const double *den, double scale,
+                const float *Wold, int j0, int j1, float *Wnew, double *num_out, void *ws, cudaStream_t st) {
+    SpecGeom g = spec_geom(m);
+    char *p = (char *)ws;
+    auto take = [&](size_t bytes) { char *r = p; p += align_up(bytes, 256); return r; };
+    double *cs = (double *)take((size_t)g.L * 8);
+    double *sn = (double *)take((size_t)g.L * 8);
+    const int nkeys = spec_nkeys(g);
+    double *ktab = (double *)take((size_t)nkeys * 2 * g.F * 8);
+    double *Sh = (double *)take((size_t)2 * g.F * g.ny * d * 8);
+    const int y0 = j0 / g.nx, y1 = (j1 + g.nx - 1) / g.nx, nyo = y1 - y0;
+    double *Nh = (double *)take((size_t)2 * g.F * nyo * d * 8);
+    spec_twiddle<<<(g.L + 255) / 256, 256, 0, st>>>(g.L, cs, sn);
+    note_launch();
+    spec_kernel_table<<<nkeys, 256, (size_t)g.L * 8, st>>>(g, htab, cs, sn, ktab);
+    note_launch();
+    dgemm_launch(g.ny, 2 * g.F, d, g.nx, FwdA{g, cs, sn}, FwdB{g, S, d}, FwdEp{g, Sh, d}, st);
+    dgemm_launch(g.F, 2 * nyo, d, 2 * g.ny, MidA{g, ktab, y0, nyo}, MidB{g, Sh, d}, MidEp{g, Nh, nyo, d}, st);
+    dgemm_launch(nyo, g.nx, d, 2 * g.F, InvA{g, cs, sn}, InvB{g, Nh, nyo, d},
+                 InvEp{g, y0, j0, j1, d, den, scale, 1.0 - scale, Wold, Wnew, num_out}, st);
+    SOMB_LAUNCH_CHECK("spectral hood update");
+    return SOMB_OK;
+}
+
+}  // namespace somb

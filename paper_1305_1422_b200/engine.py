@@ -34,6 +34,7 @@ class EngineOptions:
     window_kappa: float = _DEF_WINDOW_KAPPA
     hypot_table: bool = True          # numpy-hypot distances for rect grids (bit parity)
     seed_prev: bool = True            # seed the screen threshold from the previous BMUs
+    conv: str = "auto"                # neighbourhood convolution: "auto", "direct", "spectral"
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -118,7 +119,7 @@ class SomEngine:
         lib = _lib.load()
         ws = max(lib.somb_codebook_ws(self.K, d), lib.somb_bmu_ws(n),
                  lib.somb_node_sums_ws(n, d, self.K),
-                 lib.somb_hood_ws(C.byref(self.cmap), self.K), 1 << 16)
+                 lib.somb_hood_ws(C.byref(self.cmap), self.K, d), 1 << 16)
         self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)
         self.window_coef = float(self.opt.window_kappa * _U16 / math.sqrt(d))
         self.screen_impl = {"tensor": 0, "simt": 1, "exact": 2}[self.opt.screen]
@@ -238,7 +239,8 @@ class SomEngine:
     def update(self, radius, scale, cutoff, neighborhood=Neighborhood.GAUSSIAN, compact=False,
                num_out=None, den_out=None, all_nodes=False):
         hood = _lib.SombHood(_lib.NBH_BUBBLE if neighborhood is Neighborhood.BUBBLE
-                             else _lib.NBH_GAUSSIAN, int(bool(compact)), float(radius), float(cutoff))
+                             else _lib.NBH_GAUSSIAN, int(bool(compact)), float(radius), float(cutoff),
+                             {"auto": 0, "direct": 1, "spectral": 2}[self.opt.conv], 0)
         nb, ne = (0, self.K) if all_nodes else (self.node_begin, self.node_end)
         _lib.call("somb_hood_update", _ptr(self.S), _ptr(self.cnt), self.d, C.byref(self.cmap),
                   C.byref(hood), C.c_double(scale), _ptr(self.dist_tab), _ptr(self.W), nb, ne,

@@ -112,10 +112,11 @@ def test_node_sums_bit_exact_vs_oracle():
         np.testing.assert_allclose(got_s, s, rtol=1e-13)
 
 
+@pytest.mark.parametrize("conv", ["direct", "spectral"])
 @pytest.mark.parametrize("grid", [O.RECT, O.HEX])
 @pytest.mark.parametrize("nbh,compact", [(O.GAUSSIAN, False), (O.GAUSSIAN, True), (O.BUBBLE, False)])
 @pytest.mark.parametrize("mt", [O.PLANAR, O.TOROID])
-def test_hood_update_vs_oracle(grid, nbh, compact, mt):
+def test_hood_update_vs_oracle(grid, nbh, compact, mt, conv):
     rng = np.random.default_rng(5)
     nx, ny, d = 13, 10, 11
     k = nx * ny
@@ -125,7 +126,8 @@ def test_hood_update_vs_oracle(grid, nbh, compact, mt):
     w = rng.random((k, d), dtype=np.float32)
     x = rng.random((4, d), dtype=np.float32)
     eng = S.SomEngine(S.DenseDataset(x), nx, ny, S.MapType(mt),
-                      S.GridType.HEXAGONAL if grid == O.HEX else S.GridType.RECTANGULAR)
+                      S.GridType.HEXAGONAL if grid == O.HEX else S.GridType.RECTANGULAR,
+                      options=EngineOptions(conv=conv))
     eng.set_codebook(w)
     eng.S.copy_(torch.from_numpy(s))
     eng.cnt.copy_(torch.from_numpy(c))
@@ -136,11 +138,40 @@ def test_hood_update_vs_oracle(grid, nbh, compact, mt):
         eng.update(radius, 0.4, 1e-3, S.Neighborhood(nbh), compact, num_out=num, den_out=den,
                    all_nodes=True)
         wn, wd = O.conv_update(s, c, nx, ny, radius, 1e-3, mt, grid, nbh, compact)
-        np.testing.assert_allclose(num.cpu().numpy(), wn, rtol=1e-12, atol=1e-300)
+        got = num.cpu().numpy()
+        if conv == "direct":
+            np.testing.assert_allclose(got, wn, rtol=1e-12, atol=1e-300)
+        else:   # DFT rounding is relative to the row's scale, not per entry
+            np.testing.assert_allclose(got, wn, rtol=1e-12, atol=1e-13 * np.abs(wn).max())
         np.testing.assert_allclose(den.cpu().numpy(), wd, rtol=1e-12, atol=1e-300)
         assert np.array_equal(den.cpu().numpy() > 0, wd > 0)
         want_w = O.blend(w, wn, wd, 0.4)
-        np.testing.assert_array_max_ulp(eng.codebook(), want_w, maxulp=1)
+        np.testing.assert_array_max_ulp(eng.codebook(), want_w, maxulp=1 if conv == "direct" else 2)
+
+
+@pytest.mark.parametrize("mt", [O.PLANAR, O.TOROID])
+@pytest.mark.parametrize("grid", [O.RECT, O.HEX])
+def test_spectral_conv_large_map(mt, grid):
+    """Spectral path on a map big enough for `auto` to pick it, vs the oracle."""
+    rng = np.random.default_rng(8)
+    nx, ny, d = 64, 40, 37
+    k = nx * ny
+    c = rng.integers(0, 6, k).astype(np.float64)
+    s = rng.random((k, d)) * c[:, None]
+    w = rng.random((k, d), dtype=np.float32)
+    eng = S.SomEngine(S.DenseDataset(rng.random((4, d), dtype=np.float32)), nx, ny, S.MapType(mt),
+                      S.GridType.HEXAGONAL if grid == O.HEX else S.GridType.RECTANGULAR)
+    eng.S.copy_(torch.from_numpy(s))
+    eng.cnt.copy_(torch.from_numpy(c))
+    for radius in (1.5, 6.0, 32.0):
+        num = torch.empty((k, d), dtype=torch.float64, device=eng.dev)
+        den = torch.empty(k, dtype=torch.float64, device=eng.dev)
+        eng.set_codebook(w)
+        eng.update(radius, 0.5, 1e-3, num_out=num, den_out=den, all_nodes=True)
+        wn, wd = O.conv_update(s, c, nx, ny, radius, 1e-3, mt, grid)
+        np.testing.assert_allclose(num.cpu().numpy(), wn, rtol=1e-11, atol=1e-13 * np.abs(wn).max())
+        assert np.array_equal(den.cpu().numpy(), wd) or np.allclose(den.cpu().numpy(), wd, rtol=1e-13)
+        np.testing.assert_allclose(eng.codebook(), O.blend(w, wn, wd, 0.5), rtol=2e-7)
 
 
 def test_umatrix_golden_and_hex():
