@@ -167,6 +167,98 @@ __global__ void rerank_kernel(const float *__restrict__ X, const double *__restr
     }
 }
 
+// Vectorised re-rank for d % 4 == 0, d <= 128 * Q: the row lives in
+// registers (float4 per lane); candidate indices are fetched once (lane q
+// holds candidate q) and broadcast by shuffle; the next candidate's codebook
+// row is prefetched while the current one is reduced.  Bound by L2 traffic
+// (one 4d-byte codebook row per candidate).
+template <int Q>
+__device__ __forceinline__ void load_row4(const float *W, int64_t j, int d4, int lane, float4 (&w)[Q]) {
+    const float4 *wr = reinterpret_cast<const float4 *>(W + j * (int64_t)(d4 * 4));
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        int e = lane + 32 * q;
+        w[q] = e < d4 ? __ldg(wr + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+template <int Q, int MODE>
+__device__ __forceinline__ double dist_part(const float4 (&x)[Q], const float4 (&w)[Q]) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (MODE == SOMB_DIST_NAIVE) {
+            double a = (double)w[q].x - (double)x[q].x, b = (double)w[q].y - (double)x[q].y;
+            double c = (double)w[q].z - (double)x[q].z, e = (double)w[q].w - (double)x[q].w;
+            s = __fma_rn(a, a, s); s = __fma_rn(b, b, s); s = __fma_rn(c, c, s); s = __fma_rn(e, e, s);
+        } else {
+            s = __fma_rn((double)x[q].x, (double)w[q].x, s);
+            s = __fma_rn((double)x[q].y, (double)w[q].y, s);
+            s = __fma_rn((double)x[q].z, (double)w[q].z, s);
+            s = __fma_rn((double)x[q].w, (double)w[q].w, s);
+        }
+    }
+    return s;
+}
+
+template <int Q, int MODE>
+__global__ void __launch_bounds__(256, 2)
+rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n, int d,
+                  const float *__restrict__ W, const double *__restrict__ w2, int K,
+                  const int *__restrict__ cand, const int *__restrict__ ccount, int split,
+                  int *__restrict__ bmu, double *__restrict__ d2min) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const int d4 = d >> 2;
+    float4 xv[Q];
+    load_row4<Q>(X, row, d4, lane, xv);
+    const int cc = ccount[row];
+    const int c0 = split ? (cc & 255) : cc;
+    const int c1 = split ? ((cc >> 8) & 255) : 0;
+    int cnt = c0 + c1;
+    int myj = -1;
+    if (lane < cnt) myj = cand[row * SOMB_CAND_CAP + (lane < c0 ? lane : SOMB_CAND_CAP / 2 + (lane - c0))];
+    const bool all = cnt <= 0;       // safety net: exact scan of every node
+    if (all) cnt = K;
+    const double xx = x2[row];
+    double best = INFINITY;
+    int bestj = 0x7fffffff;
+    int j = all ? 0 : __shfl_sync(0xffffffffu, myj, 0);
+    float4 wv[Q];
+    load_row4<Q>(W, (unsigned)j < (unsigned)K ? j : 0, d4, lane, wv);
+    for (int q = 0; q < cnt; ++q) {
+        const int jn = (q + 1 < cnt) ? (all ? q + 1 : __shfl_sync(0xffffffffu, myj, q + 1)) : j;
+        float4 wn[Q];
+        load_row4<Q>(W, (unsigned)jn < (unsigned)K ? jn : 0, d4, lane, wn);   // prefetch next
+        double s = warp_sum(dist_part<Q, MODE>(xv, wv));
+        double v = s;
+        if (MODE == SOMB_DIST_BLOCKED)   // ((-2 dot) + |x|^2) + |w|^2, clamp (kernels.py:196-202)
+            v = fmax(__dadd_rn(__dadd_rn(__dmul_rn(-2.0, s), xx), w2[(unsigned)j < (unsigned)K ? j : 0]), 0.0);
+        if ((unsigned)j < (unsigned)K && (v < best || (v == best && j < bestj))) {
+            best = v;
+            bestj = j;
+        }
+        j = jn;
+#pragma unroll
+        for (int t = 0; t < Q; ++t) wv[t] = wn[t];
+    }
+    if (lane == 0) {
+        bmu[row] = bestj;
+        d2min[row] = best;
+    }
+}
+
+template <int Q>
+static void launch_rerank_vec(unsigned blocks, cudaStream_t st, const float *X, const double *x2, int64_t n, int d,
+                              const float *W, const double *w2, int K, const int *cand, const int *ccount, int mode,
+                              int split, int *bmu, double *d2min) {
+    if (mode == SOMB_DIST_NAIVE)
+        rerank_vec_kernel<Q, SOMB_DIST_NAIVE><<<blocks, 256, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, split, bmu, d2min);
+    else
+        rerank_vec_kernel<Q, SOMB_DIST_BLOCKED><<<blocks, 256, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, split, bmu, d2min);
+}
+
 // --------------------------------------------------------- qe reduction
 constexpr int kQeTile = 4096;
 
@@ -250,8 +342,20 @@ extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int3
     int all = screen_impl == 2, split = screen_impl == 0;
     if (all) cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
     const int wpb = 8;
-    rerank_kernel<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
-        X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, split, bmu, d2min);
+    const unsigned blocks = (unsigned)((n + wpb - 1) / wpb);
+    if (!all && d % 4 == 0 && d <= 1024) {
+        if (d <= 128)
+            launch_rerank_vec<1>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, bmu, d2min);
+        else if (d <= 256)
+            launch_rerank_vec<2>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, bmu, d2min);
+        else if (d <= 512)
+            launch_rerank_vec<4>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, bmu, d2min);
+        else
+            launch_rerank_vec<8>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, bmu, d2min);
+    } else {
+        rerank_kernel<<<blocks, 32 * wpb, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, split, bmu,
+                                                   d2min);
+    }
     note_launch();
     SOMB_LAUNCH_CHECK("rerank");
     return SOMB_OK;

@@ -2,38 +2,56 @@
 // tensor cores, with the per-row candidate window fused into the epilogue so
 // the N x K distance matrix never leaves the SM.
 //
-// Persistent CTAs, one per SM, warp-specialised:
-//   warp 0      TMA producer: A = 128 data rows x 64 features, B = 256 nodes x
-//               64 features (fp16, SWIZZLE_128B, K-major) into a 4-stage ring
-//   warp 1      TMEM owner + single-thread tcgen05.mma.cta_group::1.kind::f16
-//               (M=128, N=256, K=16), fp32 accumulators in TMEM, two 256-col
-//               accumulator stages (all 512 columns) so the epilogue of tile
-//               t overlaps the MMAs of tile t+1
+// Persistent, warp-specialised CTAs; template CG = CTA-group size:
+//   CG = 2 (default): CTA pairs (cluster 2x1) run tcgen05.mma.cta_group::2
+//     with M = 256 (128 data rows per CTA) x N = 256 nodes.  Each CTA
+//     TMA-loads its own 128 rows and HALF (128 nodes) of every codebook tile,
+//     so a pair moves 64 KB per 64-feature stage for 4.2M MACs -- one third
+//     fewer operand bytes per MAC than CG = 1, which matters because the
+//     screen is L2-bandwidth bound (profiles/).  Both CTAs' TMAs complete on
+//     the leader's full barrier; the leader's single MMA thread issues the
+//     pair MMA and multicasts its commits to both CTAs' empty / tmem-full
+//     barriers; both epilogues release the accumulator on the leader's
+//     tmem-empty barrier.
+//   CG = 1: one CTA per SM, M = 128 x N = 256 (kept for A/B testing).
+// Warp roles (per CTA):
+//   warp 0      TMA producer (SWIZZLE_128B, K-major fp16 tiles, S-stage ring)
+//   warp 1      TMEM owner (512 columns = two 256-column fp32 accumulator
+//               stages, so the epilogue of tile t overlaps the MMAs of t+1);
+//               lane 0 of the leader issues tcgen05.mma (K = 16 per op)
 //   warps 2..9  epilogue: tcgen05.ld 32x32b.x32 -> r = fma(acc, m, c_j) ->
 //               window candidate set (cand.cuh).  Warp w owns TMEM lane
-//               quadrant w % 4 (rows 32(w%4)..+31) and column half (w-2)/4.
-// A CTA sweeps all node tiles of one 128-row block before moving on, so each
-// row's running minimum / candidate buffer lives in registers + smem for the
-// whole sweep and is written out once.
+//               quadrant w % 4 and the interleaved 32-column chunks
+//               (w-2)/4, +2, +4, +6 of each tile.
+// A CTA sweeps all node tiles of its rows before moving on, so each row's
+// running minimum / candidate buffer lives in registers + smem for the whole
+// sweep and is written out once.
 #include <cuda.h>
 
 #include "cand.cuh"
 
 namespace somb {
 
-constexpr int TC_BM = 128;         // rows per CTA tile (UMMA M)
 constexpr int TC_BN = 256;         // nodes per tile (UMMA N)
 constexpr int TC_BK = 64;          // fp16 features per stage (one 128B swizzle atom)
-constexpr int TC_STAGES = 4;
 constexpr int TC_UMMA_K = 16;
 constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_THREADS = 32 * (2 + TC_EPI_WARPS);
-constexpr int TC_HALF_CAP = SOMB_CAND_CAP / 2;   // candidates per (row, column half)
-constexpr uint32_t TC_A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
-constexpr uint32_t TC_B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
-constexpr uint32_t TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
+constexpr int TC_HALF_CAP = SOMB_CAND_CAP / 2;   // candidates per (row, column group)
+constexpr int TC_ROWS = 128;                      // data rows per CTA (TMEM lanes)
 constexpr uint32_t TC_CAND_BYTES = TC_EPI_WARPS * 32 * TC_HALF_CAP * 8;
-constexpr uint32_t TC_SMEM = TC_STAGES * TC_STAGE_BYTES + TC_CAND_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+template <int CG>
+struct TcCfg {
+    static constexpr int B_ROWS = TC_BN / CG;                      // codebook rows loaded per CTA
+    static constexpr uint32_t A_BYTES = TC_ROWS * TC_BK * 2;       // 16 KB
+    static constexpr uint32_t B_BYTES = B_ROWS * TC_BK * 2;        // 32 KB (CG 1) / 16 KB (CG 2)
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = CG == 2 ? 6 : 4;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + TC_CAND_BYTES + 1024 + 256;
+    // kind::f16 instruction descriptor: A,B = f16, D = f32, K-major, M = 128 CG, N = 256
+    static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((128 * CG) >> 4) << 24);
+};
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -54,35 +72,70 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// arrive on the barrier at the same offset in cluster CTA `cta`
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar, uint32_t cta) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(cta));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 
+template <int CG>
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-        : "memory");
+    if constexpr (CG == 1) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+            : "memory");
+    } else {
+        // the transaction bytes land on the LEADER CTA's barrier (peer bit cleared)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+            : "memory");
+    }
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+template <int CG>
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+    if constexpr (CG == 1) {
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+    } else {
+        const uint16_t mask = 0x3;   // both CTAs of the pair, same barrier offset
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+            "h"(mask)
+            : "memory");
+    }
 }
 
+template <int CG>
 __device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-        : "memory");
+    if constexpr (CG == 1) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+            : "memory");
+    }
 }
 
 // K-major, SWIZZLE_128B smem matrix descriptor: 8-row groups 1024 B apart.
@@ -95,10 +148,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
     return d;
 }
-
-// kind::f16 instruction descriptor: A,B = f16, D = f32, both K-major, M=128, N=256
-constexpr uint32_t TC_IDESC = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
-                              ((uint32_t)(TC_BM >> 4) << 24);
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
@@ -117,50 +166,74 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ kernel
-__global__ void __launch_bounds__(TC_THREADS, 1)
-screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
-                 int64_t n, int dp, int kp, const float *__restrict__ c, const float *__restrict__ xnorm,
-                 const float *__restrict__ scal, float wcoef, const float *__restrict__ thr0,
-                 int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags,
-                 float *__restrict__ dump) {
+template <int CG>
+__device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const CUtensorMap *map_w, int64_t n,
+                                               int dp, int kp, const float *__restrict__ c,
+                                               const float *__restrict__ xnorm, const float *__restrict__ scal,
+                                               float wcoef, const float *__restrict__ thr0, int *__restrict__ cand,
+                                               int *__restrict__ ccount, int *__restrict__ flags,
+                                               float *__restrict__ dump) {
+    using Cfg = TcCfg<CG>;
+    constexpr int S = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t *sA = smem;                                     // [stage][16 KB]
-    uint8_t *sB = smem + TC_STAGES * TC_A_BYTES;            // [stage][32 KB]
-    float *cbv = (float *)(smem + TC_STAGES * TC_STAGE_BYTES);
+    uint8_t *sA = smem;                                     // [stage][A_BYTES]
+    uint8_t *sB = smem + S * Cfg::A_BYTES;                  // [stage][B_BYTES]
+    float *cbv = (float *)(smem + S * Cfg::STAGE_BYTES);
     int *cbi = (int *)(cbv + TC_EPI_WARPS * 32 * TC_HALF_CAP);
-    uint64_t *bars = (uint64_t *)(smem + TC_STAGES * TC_STAGE_BYTES + TC_CAND_BYTES);
+    uint64_t *bars = (uint64_t *)(smem + S * Cfg::STAGE_BYTES + TC_CAND_BYTES);
     // bars: full[S] empty[S] tfull[2] tempty[2]; then the TMEM base address
-    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * TC_STAGES + 4);
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * S + 4);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TC_STAGES);
-    const uint32_t tfull0 = smem_u32(bars + 2 * TC_STAGES), tempty0 = smem_u32(bars + 2 * TC_STAGES + 2);
+    const uint32_t crank = CG == 2 ? cluster_rank() : 0;
+    const bool leader = crank == 0;
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
+    const uint32_t tfull0 = smem_u32(bars + 2 * S), tempty0 = smem_u32(bars + 2 * S + 2);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TC_STAGES; ++s) {
+        for (int s = 0; s < S; ++s) {
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull0 + 8 * a, 1);
-            mbar_init(tempty0 + 8 * a, 32 * TC_EPI_WARPS);
+            mbar_init(tempty0 + 8 * a, CG * TC_EPI_WARPS);   // one arrival per epilogue warp of the pair
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map_x)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map_w)) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();   // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int num_rb = (int)((n + TC_BM - 1) / TC_BM);
+    // work unit: a block of 128*CG rows; this CTA owns rows [unit*128*CG + 128*crank, +128)
+    const int unit_rows = TC_ROWS * CG;
+    const int num_units = (int)((n + unit_rows - 1) / unit_rows);
+    const int unit0 = blockIdx.x / CG, unit_step = gridDim.x / CG;
     const int NT = kp / TC_BN;
     const int KB = (dp + TC_BK - 1) / TC_BK;
 
@@ -168,26 +241,28 @@ screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int rb = blockIdx.x; rb < num_rb; rb += gridDim.x) {
+            for (int u = unit0; u < num_units; u += unit_step) {
+                const int row0 = u * unit_rows + TC_ROWS * (int)crank;
                 for (int nt = 0; nt < NT; ++nt) {
+                    const int node0 = nt * TC_BN + Cfg::B_ROWS * (int)crank;
                     for (int kb = 0; kb < KB; ++kb) {
                         mbar_wait(empty0 + 8 * stage, phase ^ 1);
                         const uint32_t fb = full0 + 8 * stage;
-                        mbar_expect_tx(fb, TC_STAGE_BYTES);
-                        tma_load_2d(smem_u32(sA + stage * TC_A_BYTES), &map_x, fb, kb * TC_BK, rb * TC_BM);
-                        tma_load_2d(smem_u32(sB + stage * TC_B_BYTES), &map_w, fb, kb * TC_BK, nt * TC_BN);
-                        if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                        if (leader) mbar_expect_tx(fb, CG * Cfg::STAGE_BYTES);
+                        tma_load_2d<CG>(smem_u32(sA + stage * Cfg::A_BYTES), map_x, fb, kb * TC_BK, row0);
+                        tma_load_2d<CG>(smem_u32(sB + stage * Cfg::B_BYTES), map_w, fb, kb * TC_BK, node0);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (leader && lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t aphase = 0;
-            for (int rb = blockIdx.x; rb < num_rb; rb += gridDim.x) {
+            for (int u = unit0; u < num_units; u += unit_step) {
                 for (int nt = 0; nt < NT; ++nt) {
                     mbar_wait(tempty0 + 8 * acc, aphase ^ 1);
                     tc_fence_after();
@@ -195,17 +270,17 @@ screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                     for (int kb = 0; kb < KB; ++kb) {
                         mbar_wait(full0 + 8 * stage, phase);
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(sA + stage * TC_A_BYTES);
-                        const uint32_t b0 = smem_u32(sB + stage * TC_B_BYTES);
+                        const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+                        const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
 #pragma unroll
                         for (int k = 0; k < TC_BK / TC_UMMA_K; ++k) {
-                            tc_mma_f16(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), TC_IDESC,
-                                       (kb | k) != 0);
+                            tc_mma_f16<CG>(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), Cfg::IDESC,
+                                           (kb | k) != 0);
                         }
-                        tc_commit(empty0 + 8 * stage);   // frees the smem slot when these MMAs retire
-                        if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                        tc_commit<CG>(empty0 + 8 * stage);   // frees the smem slot(s) when these MMAs retire
+                        if (++stage == S) { stage = 0; phase ^= 1; }
                     }
-                    tc_commit(tfull0 + 8 * acc);         // accumulator ready for the epilogue
+                    tc_commit<CG>(tfull0 + 8 * acc);         // accumulator ready for the epilogue(s)
                     if (++acc == 2) { acc = 0; aphase ^= 1; }
                 }
             }
@@ -224,8 +299,8 @@ screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
         const CandBuf cb{smem_u32(cbv + et), smem_u32(cbi + et), 4u * TC_EPI_WARPS * 32};
         int acc = 0;
         uint32_t aphase = 0;
-        for (int rb = blockIdx.x; rb < num_rb; rb += gridDim.x) {
-            const int64_t row = (int64_t)rb * TC_BM + quad * 32 + lane;
+        for (int u = unit0; u < num_units; u += unit_step) {
+            const int64_t row = (int64_t)u * unit_rows + TC_ROWS * crank + quad * 32 + lane;
             const bool live = row < n;
             CandRow<TC_HALF_CAP> st;
             cand_init(st, live ? wcoef * xnorm[row] * nmax : 0.0f);
@@ -263,13 +338,17 @@ screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(tempty0 + 8 * acc);
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 1 || leader) mbar_arrive_local(tempty0 + 8 * acc);
+                    else mbar_arrive_cluster(tempty0 + 8 * acc, 0);
+                }
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
             if (live) {
                 int *out = cand + row * SOMB_CAND_CAP + half * TC_HALF_CAP;
                 int cnt = cand_emit<TC_HALF_CAP>(st, cb, out);
-                // two halves write disjoint bytes of ccount / flags
+                // two column groups write disjoint bytes of ccount / flags
                 reinterpret_cast<uint8_t *>(ccount + row)[half] = (uint8_t)cnt;
                 reinterpret_cast<uint8_t *>(flags + row)[half] = (uint8_t)st.trunc;
             }
@@ -277,10 +356,28 @@ screen_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();      // no CTA leaves while its peer's MMAs may target it
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+        if constexpr (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
+}
+
+#define SCREEN_TC_ARGS                                                                                              \
+    const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, int64_t n, int dp, int kp, \
+        const float *__restrict__ c, const float *__restrict__ xnorm, const float *__restrict__ scal, float wcoef,  \
+        const float *__restrict__ thr0, int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags,  \
+        float *__restrict__ dump
+
+__global__ void __launch_bounds__(TC_THREADS, 1) screen_tc1_kernel(SCREEN_TC_ARGS) {
+    screen_tc_body<1>(&map_x, &map_w, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount, flags, dump);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) screen_tc2_kernel(SCREEN_TC_ARGS) {
+    screen_tc_body<2>(&map_x, &map_w, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount, flags, dump);
 }
 
 // --------------------------------------------------------------- host side
@@ -314,30 +411,44 @@ static int make_map(CUtensorMap *map, const void *base, uint64_t inner, uint64_t
     return SOMB_OK;
 }
 
+static int g_tc_group = 2;   // SOMB_TC_GROUP=1 selects the single-CTA variant (A/B testing)
+
 int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int kp, const float *c,
                      const float *xnorm, const float *scal, float wcoef, const float *thr0, int *cand,
                      int *ccount, int *flags, float *dump, cudaStream_t st) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % TC_BN == 0, SOMB_E_INPUT, "screen_tc: dp %% 8 and kp %% 256 required");
-    CUtensorMap mx, mw;
-    int rc = make_map(&mx, Xh, (uint64_t)dp, (uint64_t)n, TC_BM);
-    if (rc) return rc;
-    rc = make_map(&mw, Wh, (uint64_t)dp, (uint64_t)kp, TC_BN);
-    if (rc) return rc;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(screen_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-        if (e != cudaSuccess) return cuda_status(e, "screen_tc smem attribute");
-        attr_set = true;
+    static bool init = false;
+    if (!init) {
+        const char *e = getenv("SOMB_TC_GROUP");
+        if (e && atoi(e) == 1) g_tc_group = 1;
+        cudaError_t r1 = cudaFuncSetAttribute(screen_tc1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              TcCfg<1>::SMEM);
+        cudaError_t r2 = cudaFuncSetAttribute(screen_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              TcCfg<2>::SMEM);
+        if (r1 != cudaSuccess) return cuda_status(r1, "screen_tc1 smem attribute");
+        if (r2 != cudaSuccess) return cuda_status(r2, "screen_tc2 smem attribute");
+        init = true;
     }
+    const int cg = g_tc_group;
+    CUtensorMap mx, mw;
+    int rc = make_map(&mx, Xh, (uint64_t)dp, (uint64_t)n, TC_ROWS);
+    if (rc) return rc;
+    rc = make_map(&mw, Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg));
+    if (rc) return rc;
     int dev = 0, sms = kSmCount;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaMemsetAsync(ccount, 0, (size_t)n * sizeof(int), st);
     cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
-    int num_rb = (int)((n + TC_BM - 1) / TC_BM);
-    int grid = num_rb < sms ? num_rb : sms;
-    screen_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
-                                                        flags, dump);
+    const int units = (int)((n + TC_ROWS * cg - 1) / (TC_ROWS * cg));
+    const int max_units = sms / cg;
+    const int grid = cg * (units < max_units ? units : max_units);
+    if (cg == 2)
+        screen_tc2_kernel<<<grid, TC_THREADS, TcCfg<2>::SMEM, st>>>(mx, mw, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand,
+                                                                     ccount, flags, dump);
+    else
+        screen_tc1_kernel<<<grid, TC_THREADS, TcCfg<1>::SMEM, st>>>(mx, mw, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand,
+                                                                     ccount, flags, dump);
     note_launch();
     SOMB_LAUNCH_CHECK("screen_tc");
     return SOMB_OK;
