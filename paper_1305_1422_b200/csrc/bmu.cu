@@ -15,9 +15,10 @@ int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int 
                      cudaStream_t st);
 
 // Seed of each row's acceptance threshold from its previous BMU: the screened
-// value of that node (same fp16 operands, fp32 FMA) plus two windows of slack
-// (covers the summation-order difference to the tensor-core value; the
-// window already exceeds twice the screen error).  Any node the screen will
+// value of that node (same fp16 operands, fp32 FMA) plus one window and an
+// eighth (the extra eighth covers the summation-order difference to the
+// tensor-core value of the same node, which is orders of magnitude below the
+// window).  Any node the screen will
 // keep has r <= r_min + win <= r_prev + win, so seeding never changes the
 // final candidate set -- it only skips transient pushes (cand.cuh).
 __global__ void screen_seed_kernel(const __half *__restrict__ Xh, int64_t n, int dp,
@@ -42,7 +43,7 @@ __global__ void screen_seed_kernel(const __half *__restrict__ Xh, int64_t n, int
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         float r = fmaf(acc, scal[0], c[j]);
         float win = wcoef * xnorm[row] * scal[1];
-        if (r < FLT_MAX) t = r + 2.0f * win;
+        if (r < FLT_MAX) t = r + 1.125f * win;
     }
     if (lane == 0) thr0[row] = t;
 }

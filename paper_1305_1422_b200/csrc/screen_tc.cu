@@ -176,6 +176,11 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// 0 = normal; 1 = profiling mode (epilogue releases accumulators without
+// reading them: measures the TMA + tcgen05 feed alone).  Set from the
+// SOMB_SCREEN_PROFILE environment variable.
+__constant__ int g_profile_mode = 0;
+
 // ------------------------------------------------------------------ kernel
 template <int CG>
 __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const CUtensorMap *map_w, int64_t n,
@@ -309,6 +314,15 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             for (int nt = 0; nt < NT; ++nt) {
                 mbar_wait(tfull0 + 8 * acc, aphase);
                 tc_fence_after();
+                if (g_profile_mode == 1) {   // profiling: release the accumulator untouched
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (CG == 1 || leader) mbar_arrive_local(tempty0 + 8 * acc);
+                        else mbar_arrive_cluster(tempty0 + 8 * acc, 0);
+                    }
+                    if (++acc == 2) { acc = 0; aphase ^= 1; }
+                    continue;
+                }
                 const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN);
 #pragma unroll 1
                 for (int ch = half; ch < TC_BN / 32; ch += 2) {
@@ -316,7 +330,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     tmem_ld32(tbase + ch * 32, v);
                     const int jc = nt * TC_BN + ch * 32;
                     const float4 *cp = reinterpret_cast<const float4 *>(c + jc);
-                    float lo = INFINITY;
+                    float gmin[4];   // minima of the four 8-column groups
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         float4 cc = __ldg(cp + q);
@@ -324,17 +338,24 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         v[4 * q + 1] = fmaf(v[4 * q + 1], m, cc.y);
                         v[4 * q + 2] = fmaf(v[4 * q + 2], m, cc.z);
                         v[4 * q + 3] = fmaf(v[4 * q + 3], m, cc.w);
-                        lo = fminf(lo, fminf(fminf(v[4 * q], v[4 * q + 1]), fminf(v[4 * q + 2], v[4 * q + 3])));
+                        float l4 = fminf(fminf(v[4 * q], v[4 * q + 1]), fminf(v[4 * q + 2], v[4 * q + 3]));
+                        gmin[q >> 1] = (q & 1) ? fminf(gmin[q >> 1], l4) : l4;
                     }
                     if (dumping) {
 #pragma unroll
                         for (int q = 0; q < 32; ++q) dump[row * kp + jc + q] = v[q];
                     }
+                    const float lo = fminf(fminf(gmin[0], gmin[1]), fminf(gmin[2], gmin[3]));
                     if (live && lo <= st.thr) {
                         cand_bound(st, lo);   // the chunk minimum is about to be pushed
 #pragma unroll
-                        for (int q = 0; q < 32; ++q)
-                            if (v[q] <= st.thr) cand_push<TC_HALF_CAP>(st, v[q], jc + q, cb);
+                        for (int g8 = 0; g8 < 4; ++g8) {
+                            if (gmin[g8] <= st.thr) {
+#pragma unroll
+                                for (int q = 8 * g8; q < 8 * g8 + 8; ++q)
+                                    if (v[q] <= st.thr) cand_push<TC_HALF_CAP>(st, v[q], jc + q, cb);
+                            }
+                        }
                     }
                 }
                 tc_fence_before();
@@ -421,6 +442,9 @@ int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int 
     if (!init) {
         const char *e = getenv("SOMB_TC_GROUP");
         if (e && atoi(e) == 1) g_tc_group = 1;
+        const char *pm = getenv("SOMB_SCREEN_PROFILE");
+        int mode = pm ? atoi(pm) : 0;
+        cudaMemcpyToSymbol(g_profile_mode, &mode, sizeof(int));
         cudaError_t r1 = cudaFuncSetAttribute(screen_tc1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               TcCfg<1>::SMEM);
         cudaError_t r2 = cudaFuncSetAttribute(screen_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
