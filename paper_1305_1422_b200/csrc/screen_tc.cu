@@ -103,6 +103,30 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
     }
 }
 
+// Same with an L2 cache policy (createpolicy): the CTA's own data rows are
+// re-read for every node tile of its sweep, so they are loaded evict_last.
+template <int CG>
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
+                                                 uint64_t pol) {
+    if constexpr (CG == 1) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
+            : "memory");
+    } else {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "l"(pol)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -180,6 +204,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 // reading them: measures the TMA + tcgen05 feed alone).  Set from the
 // SOMB_SCREEN_PROFILE environment variable.
 __constant__ int g_profile_mode = 0;
+// 1 = load the data-row (A) tiles with an L2 evict_last policy (SOMB_A_EVICT_LAST, default 0: measured no gain at cfg2)
+__constant__ int g_a_evict_last = 0;
 
 // ------------------------------------------------------------------ kernel
 template <int CG>
@@ -244,6 +270,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
 
     if (warp == 0) {
         if (lane == 0) {
+            const uint64_t pol_a = policy_evict_last();
+            const bool hint_a = g_a_evict_last != 0;
             int stage = 0;
             uint32_t phase = 0;
             for (int u = unit0; u < num_units; u += unit_step) {
@@ -254,7 +282,10 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         mbar_wait(empty0 + 8 * stage, phase ^ 1);
                         const uint32_t fb = full0 + 8 * stage;
                         if (leader) mbar_expect_tx(fb, CG * Cfg::STAGE_BYTES);
-                        tma_load_2d<CG>(smem_u32(sA + stage * Cfg::A_BYTES), map_x, fb, kb * TC_BK, row0);
+                        if (hint_a)
+                            tma_load_2d_hint<CG>(smem_u32(sA + stage * Cfg::A_BYTES), map_x, fb, kb * TC_BK, row0, pol_a);
+                        else
+                            tma_load_2d<CG>(smem_u32(sA + stage * Cfg::A_BYTES), map_x, fb, kb * TC_BK, row0);
                         tma_load_2d<CG>(smem_u32(sB + stage * Cfg::B_BYTES), map_w, fb, kb * TC_BK, node0);
                         if (++stage == S) { stage = 0; phase ^= 1; }
                     }
@@ -445,6 +476,9 @@ int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int 
         const char *pm = getenv("SOMB_SCREEN_PROFILE");
         int mode = pm ? atoi(pm) : 0;
         cudaMemcpyToSymbol(g_profile_mode, &mode, sizeof(int));
+        const char *ae = getenv("SOMB_A_EVICT_LAST");
+        int a_last = ae ? atoi(ae) : 0;
+        cudaMemcpyToSymbol(g_a_evict_last, &a_last, sizeof(int));
         cudaError_t r1 = cudaFuncSetAttribute(screen_tc1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               TcCfg<1>::SMEM);
         cudaError_t r2 = cudaFuncSetAttribute(screen_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
