@@ -233,8 +233,8 @@ class SomEngine:
 
     def reduce(self):
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(self.acc, op=dist.ReduceOp.SUM, group=self.group)
+            from .parallel import allreduce_sum
+            allreduce_sum(self.acc, self.group)
 
     def update(self, radius, scale, cutoff, neighborhood=Neighborhood.GAUSSIAN, compact=False,
                num_out=None, den_out=None, all_nodes=False):
@@ -246,10 +246,8 @@ class SomEngine:
                   C.byref(hood), C.c_double(scale), _ptr(self.dist_tab), _ptr(self.W), nb, ne,
                   _ptr(self.W2), _ptr(num_out), _ptr(den_out), _ptr(self.ws), _stream(self.dev))
         if self.world > 1 and not all_nodes:
-            import torch.distributed as dist
-            lo = self.rank * self.kc
-            dist.all_gather_into_tensor(self.W2, self.W2[lo: lo + self.kc].contiguous(),
-                                        group=self.group)
+            from .parallel import allgather_rows
+            allgather_rows(self.W2, self.kc, self.group)
         self.W, self.W2 = self.W2, self.W
 
     def epoch(self, radius, scale, cutoff, neighborhood=Neighborhood.GAUSSIAN, compact=False):
