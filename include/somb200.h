@@ -84,10 +84,11 @@ SOMB_API int somb_device_check(int dev);
 SOMB_API size_t somb_data_stats_ws(int32_t d);
 SOMB_API int somb_data_stats(const float *X, int64_t n, int32_t d, float *nu,
                     float *absmax /* [1] max|x - nu| */, void *ws, void *stream);
-/* Xh[i][k] = fp16((x_ik - nu_k) * 2^xexp) (pitch dp, zero pad); xnorm[i] =
- * |x_i - nu|_2 (f32); x2[i] = |x_i|^2 in fp64 (kernels.py:198). */
+/* Xh[i][k] = fp16((x_ik - nu_k) * 2^xexp) (pitch dp, zero pad); Xl (may be
+ * NULL) = fp16 residual of that rounding (enables the 3-pass screen);
+ * xnorm[i] = |x_i - nu|_2 (f32); x2[i] = |x_i|^2 in fp64 (kernels.py:198). */
 SOMB_API int somb_data_pack(const float *X, int64_t n, int32_t d, const float *nu,
-                   int32_t xexp, uint16_t *Xh, int32_t dp, float *xnorm,
+                   int32_t xexp, uint16_t *Xh, uint16_t *Xl, int32_t dp, float *xnorm,
                    double *x2, void *stream);
 
 /* ---- codebook, once per epoch ----------------------------------------
@@ -98,7 +99,7 @@ SOMB_API int somb_data_pack(const float *X, int64_t n, int32_t d, const float *n
  * device scalars consumed by somb_bmu_dense.  ws >= somb_codebook_ws(K, d). */
 SOMB_API size_t somb_codebook_ws(int32_t K, int32_t d);
 SOMB_API int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const float *nu,
-                          int32_t xexp, uint16_t *Wh, int32_t dp, int32_t kp,
+                          int32_t xexp, uint16_t *Wh, uint16_t *Wl, int32_t dp, int32_t kp,
                           float *c, double *w2, float *scal, void *ws,
                           void *stream);
 
@@ -123,15 +124,16 @@ SOMB_API int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xno
 SOMB_API size_t somb_bmu_ws(int64_t n);
 /* prev_bmu (may be NULL): each row's BMU from the previous search; seeds the
  * screening threshold (does not change the result, only the work). */
-SOMB_API int somb_bmu_screen(const uint16_t *Xh, const float *xnorm, int64_t n,
-                             int32_t dp, const uint16_t *Wh, const float *c,
+/* Xl / Wl (both non-NULL): 3-pass split screen hi.hi + hi.lo + lo.hi. */
+SOMB_API int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm, int64_t n,
+                             int32_t dp, const uint16_t *Wh, const uint16_t *Wl, const float *c,
                              int32_t K, int32_t kp, const float *scal,
                              float window_coef, const int32_t *prev_bmu,
                              int32_t screen_impl, int32_t *flags, void *ws,
                              void *stream);
 /* Calibration: tcgen05 screened values of rows [0, min(n,128)) x kp nodes. */
-SOMB_API int somb_debug_screen_dump(const uint16_t *Xh, const float *xnorm,
-                                    int64_t n, int32_t dp, const uint16_t *Wh,
+SOMB_API int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm,
+                                    int64_t n, int32_t dp, const uint16_t *Wh, const uint16_t *Wl,
                                     const float *c, int32_t kp, const float *scal,
                                     float window_coef, float *dump, void *ws,
                                     void *stream);

@@ -9,9 +9,9 @@
 
 namespace somb {
 
-int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int kp,
-                     const float *c, const float *xnorm, const float *scal, float wcoef,
-                     const float *thr0, int *cand, int *ccount, int *flags, float *dump,
+int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh,
+                     const __half *Wl, int kp, const float *c, const float *xnorm, const float *scal,
+                     float wcoef, const float *thr0, int *cand, int *ccount, int *flags, float *dump,
                      cudaStream_t st);
 
 // Seed of each row's acceptance threshold from its previous BMU: the screened
@@ -21,10 +21,14 @@ int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int 
 // window).  Any node the screen will
 // keep has r <= r_min + win <= r_prev + win, so seeding never changes the
 // final candidate set -- it only skips transient pushes (cand.cuh).
-__global__ void screen_seed_kernel(const __half *__restrict__ Xh, int64_t n, int dp,
-                                   const __half *__restrict__ Wh, int K, const float *__restrict__ c,
-                                   const float *__restrict__ xnorm, const float *__restrict__ scal,
-                                   float wcoef, const int *__restrict__ prev, float *__restrict__ thr0) {
+// 3-pass mode (Xl, Wl given): the seed is the fp64 value of the same split
+// product, and the slack is 1.5 windows (the tensor-core value differs from
+// it by at most the screen error, <= half a window).
+__global__ void screen_seed_kernel(const __half *__restrict__ Xh, const __half *__restrict__ Xl, int64_t n, int dp,
+                                   const __half *__restrict__ Wh, const __half *__restrict__ Wl, int K,
+                                   const float *__restrict__ c, const float *__restrict__ xnorm,
+                                   const float *__restrict__ scal, float wcoef, const int *__restrict__ prev,
+                                   float *__restrict__ thr0) {
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -33,17 +37,34 @@ __global__ void screen_seed_kernel(const __half *__restrict__ Xh, int64_t n, int
     if (j >= 0 && j < K) {
         const __half2 *x = reinterpret_cast<const __half2 *>(Xh + row * (int64_t)dp);
         const __half2 *w = reinterpret_cast<const __half2 *>(Wh + (int64_t)j * dp);
-        float acc = 0.0f;
-        for (int k = lane; k < dp / 2; k += 32) {
-            float2 a = __half22float2(x[k]), b = __half22float2(w[k]);
-            acc = fmaf(a.x, b.x, acc);
-            acc = fmaf(a.y, b.y, acc);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        float r = fmaf(acc, scal[0], c[j]);
         float win = wcoef * xnorm[row] * scal[1];
-        if (r < FLT_MAX) t = r + 1.125f * win;
+        float r;
+        if (Xl == nullptr) {
+            float acc = 0.0f;
+            for (int k = lane; k < dp / 2; k += 32) {
+                float2 a = __half22float2(x[k]), b = __half22float2(w[k]);
+                acc = fmaf(a.x, b.x, acc);
+                acc = fmaf(a.y, b.y, acc);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            r = fmaf(acc, scal[0], c[j]);
+            if (r < FLT_MAX) r += 1.125f * win;
+        } else {
+            const __half2 *xl = reinterpret_cast<const __half2 *>(Xl + row * (int64_t)dp);
+            const __half2 *wl = reinterpret_cast<const __half2 *>(Wl + (int64_t)j * dp);
+            double acc = 0.0;
+            for (int k = lane; k < dp / 2; k += 32) {
+                float2 a = __half22float2(x[k]), b = __half22float2(w[k]);
+                float2 al = __half22float2(xl[k]), bl = __half22float2(wl[k]);
+                acc += (double)a.x * b.x + (double)a.x * bl.x + (double)al.x * b.x;
+                acc += (double)a.y * b.y + (double)a.y * bl.y + (double)al.y * b.y;
+            }
+            acc = warp_sum(acc);
+            r = (float)(acc * (double)scal[0] + (double)c[j]);
+            if (r < FLT_MAX) r += 1.5f * win;
+        }
+        if (r < FLT_MAX) t = r;
     }
     if (lane == 0) thr0[row] = t;
 }
@@ -302,8 +323,8 @@ extern "C" size_t somb_bmu_ws(int64_t n) {
     return align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256) + 2 * align_up((size_t)n * sizeof(int), 256);
 }
 
-extern "C" int somb_bmu_screen(const uint16_t *Xh, const float *xnorm, int64_t n, int32_t dp,
-                               const uint16_t *Wh, const float *c, int32_t K, int32_t kp,
+extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm, int64_t n, int32_t dp,
+                               const uint16_t *Wh, const uint16_t *Wl, const float *c, int32_t K, int32_t kp,
                                const float *scal, float window_coef, const int32_t *prev_bmu,
                                int32_t screen_impl, int32_t *flags, void *ws, void *stream) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % 256 == 0, SOMB_E_INPUT, "bmu_screen: dp=%d kp=%d", dp, kp);
@@ -315,13 +336,16 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const float *xnorm, int64_t n
     float *thr0 = nullptr;
     if (prev_bmu) {
         thr0 = (float *)((char *)ccount + align_up((size_t)n * sizeof(int), 256));
-        screen_seed_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh,
-                                                                     K, c, xnorm, scal, window_coef, prev_bmu, thr0);
+        const bool three = Xl != nullptr && Wl != nullptr && screen_impl == 0;
+        screen_seed_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(
+            (const __half *)Xh, three ? (const __half *)Xl : nullptr, n, dp, (const __half *)Wh,
+            three ? (const __half *)Wl : nullptr, K, c, xnorm, scal, window_coef, prev_bmu, thr0);
         note_launch();
     }
     if (screen_impl == 0)
-        return launch_screen_tc((const __half *)Xh, n, dp, (const __half *)Wh, kp, c, xnorm, scal,
-                                window_coef, thr0, cand, ccount, flags, nullptr, st);
+        return launch_screen_tc((const __half *)Xh, (const __half *)Xl, n, dp, (const __half *)Wh,
+                                (const __half *)Wl, kp, c, xnorm, scal, window_coef, thr0, cand, ccount, flags,
+                                nullptr, st);
     unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
     screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh, kp, c,
                                                       xnorm, scal, window_coef, thr0, cand, ccount, flags);
@@ -370,8 +394,8 @@ extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *x
                               void *ws, void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && kp >= K, SOMB_E_INPUT,
                  "bmu_dense: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
-    int rc = somb_bmu_screen(Xh, xnorm, n, dp, Wh, c, K, kp, scal, window_coef, nullptr, screen_impl, flags,
-                             ws, stream);
+    int rc = somb_bmu_screen(Xh, nullptr, xnorm, n, dp, Wh, nullptr, c, K, kp, scal, window_coef, nullptr,
+                             screen_impl, flags, ws, stream);
     if (rc) return rc;
     return somb_bmu_rerank(X, x2, n, d, W, w2, K, dist_mode, screen_impl, bmu, d2min, flags, ws, stream);
 }
@@ -395,13 +419,13 @@ extern "C" int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws
 // Debug/calibration: screened values r_j of rows [0, min(n, 128)) for all kp
 // nodes from the tcgen05 kernel (dump [128][kp] f32); candidates are
 // computed as usual.  Used to measure the real screen error.
-extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const float *xnorm, int64_t n, int32_t dp,
-                                      const uint16_t *Wh, const float *c, int32_t kp, const float *scal,
-                                      float window_coef, float *dump, void *ws, void *stream) {
+extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm, int64_t n,
+                                      int32_t dp, const uint16_t *Wh, const uint16_t *Wl, const float *c, int32_t kp,
+                                      const float *scal, float window_coef, float *dump, void *ws, void *stream) {
     int64_t m = n < 128 ? n : 128;
     int *cand = (int *)ws;
     int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
     int *flags = (int *)((char *)ccount + align_up((size_t)n * sizeof(int), 256));
-    return launch_screen_tc((const __half *)Xh, m, dp, (const __half *)Wh, kp, c, xnorm, scal, window_coef,
-                            nullptr, cand, ccount, flags, dump, as_stream(stream));
+    return launch_screen_tc((const __half *)Xh, (const __half *)Xl, m, dp, (const __half *)Wh, (const __half *)Wl, kp,
+                            c, xnorm, scal, window_coef, nullptr, cand, ccount, flags, dump, as_stream(stream));
 }

@@ -178,8 +178,9 @@ hood_conv_blend(MapDev m, int tw, const double *__restrict__ htab, const double 
 
 int exclusive_scan(const int *in, int len, int *out, cudaStream_t st);
 size_t spec_ws_bytes(const somb_map *m, int d);
-int spec_update(const somb_map *m, const double *htab, const double *S, int d, const double *den, double scale,
-                const float *Wold, int j0, int j1, float *Wnew, double *num_out, void *ws, cudaStream_t st);
+int spec_update(const somb_map *m, const double *htab, const double *S, const double *cnt, int d, double *den,
+                int den_mode, double tau, double scale, const float *Wold, int j0, int j1, float *Wnew,
+                double *num_out, void *ws, cudaStream_t st);
 
 }  // namespace somb
 
@@ -245,11 +246,16 @@ extern "C" int somb_hood_update(const double *S, const double *cnt, int32_t d, c
     const int *nocc = pos + K;
     const int nn = node_end - node_begin;
     if (nn == 0) return SOMB_OK;
-    hood_den_kernel<<<(nn + 255) / 256, 256, 0, st>>>(m, tw, htab, cnt, occ, nocc, node_begin, node_end, den);
-    note_launch();
-    if (use_spectral(map, hood)) {
+    const bool spectral = use_spectral(map, hood);
+    const bool spec_den = spectral && hood->cutoff > 0.0;
+    if (!spec_den) {
+        hood_den_kernel<<<(nn + 255) / 256, 256, 0, st>>>(m, tw, htab, cnt, occ, nocc, node_begin, node_end, den);
+        note_launch();
+    }
+    if (spectral) {
         char *sws = (char *)ws + direct_ws(map, K);
-        return spec_update(map, htab, S, d, den, scale, W_old, node_begin, node_end, W_new, num_out, sws, st);
+        return spec_update(map, htab, S, cnt, d, den, spec_den ? 1 : 0, 0.5 * hood->cutoff, scale, W_old, node_begin,
+                           node_end, W_new, num_out, sws, st);
     }
     dim3 g((d + kHN - 1) / kHN, (nn + kHM - 1) / kHM);
     hood_conv_blend<<<g, 256, 0, st>>>(m, tw, htab, S, d, occ, nocc, node_begin, node_end, den, scale,

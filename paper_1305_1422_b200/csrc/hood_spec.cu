@@ -14,8 +14,11 @@
 // no wrap).  Only the F = L/2 + 1 non-redundant frequencies of the real
 // input are carried.  Every step runs in fp64 through one tiled DFMA GEMM
 // template with functional operand loaders; the influence values are the same
-// htab entries the direct path uses (hood.cu), and den (with its exact zero
-// pattern for the den > 0 blend mask) still comes from the direct fp64 sum.
+// htab entries the direct path uses (hood.cu).  den = H cnt rides along as
+// one extra channel; its exact zero pattern (the den > 0 blend mask) is
+// restored by thresholding at hmin / 2, valid whenever cutoff > 0 (every
+// nonzero influence is then >= cutoff); with cutoff = 0 the direct fp64 den
+// is used instead.
 // Cost ~ F ny^2 D + 4 K F D complex MACs instead of K^2 D.
 #include "common.cuh"
 
@@ -173,10 +176,12 @@ struct FwdA {
         return r < g.F ? cs[q] : -sn[q];
     }
 };
+// column d == D carries the BMU counts, so den = H cnt rides the same DFTs
 struct FwdB {
-    SpecGeom g; const double *S; int D;
+    SpecGeom g; const double *S; const double *cnt; int D;
     __device__ double operator()(int y, int c, int d) const {
-        return c < g.nx ? S[((int64_t)y * g.nx + c) * D + d] : 0.0;
+        if (c >= g.nx) return 0.0;
+        return d < D ? S[((int64_t)y * g.nx + c) * D + d] : cnt[y * g.nx + c];
     }
 };
 // Shat layout [plane][f][y][d]
@@ -215,6 +220,26 @@ struct MidEp {
         Nh[(((int64_t)pr * g.F + f) * nyo + yl) * D + d] = v;
     }
 };
+// inv for the count channel: den_j, with the exact zero pattern restored --
+// every nonzero influence is >= hmin (cutoff, or 1 for bubble), so a true
+// den_j is 0 or >= hmin, while the DFT rounding is orders of magnitude below
+// hmin / 2.
+struct DenB {
+    SpecGeom g; const double *Nh; int nyo, Dp1;
+    __device__ double operator()(int yl, int q2, int) const {
+        int plane = q2 >= g.F, f = q2 - plane * g.F;
+        return Nh[(((int64_t)plane * g.F + f) * nyo + yl) * Dp1 + (Dp1 - 1)];
+    }
+};
+struct DenEp {
+    SpecGeom g; int y0, j0, j1; double tau; double *den;
+    __device__ void operator()(int yl, int c, int, double v) const {
+        if (c >= g.nx) return;
+        int j = (y0 + yl) * g.nx + c;
+        if (j < j0 || j >= j1) return;
+        den[j] = v < tau ? 0.0 : v;
+    }
+};
 // inv: num_y [nx x D] = Psi [nx x 2F] * [Nr_y; Ni_y]
 struct InvA {
     SpecGeom g; const double *cs, *sn;
@@ -227,10 +252,10 @@ struct InvA {
     }
 };
 struct InvB {
-    SpecGeom g; const double *Nh; int nyo, D;
+    SpecGeom g; const double *Nh; int nyo, Dp1;
     __device__ double operator()(int yl, int q2, int d) const {
         int plane = q2 >= g.F, f = q2 - plane * g.F;
-        return Nh[(((int64_t)plane * g.F + f) * nyo + yl) * D + d];
+        return Nh[(((int64_t)plane * g.F + f) * nyo + yl) * Dp1 + d];
     }
 };
 struct InvEp {
@@ -274,13 +299,16 @@ size_t spec_ws_bytes(const somb_map *m, int d) {
     SpecGeom g = spec_geom(m);
     size_t b = 2 * align_up((size_t)g.L * 8, 256);
     b += align_up((size_t)spec_nkeys(g) * 2 * g.F * 8, 256);
-    b += align_up((size_t)2 * g.F * g.ny * d * 8, 256);      // Shat
-    b += align_up((size_t)2 * g.F * g.ny * d * 8, 256);      // Nhat (worst case: all rows)
+    b += align_up((size_t)2 * g.F * g.ny * (d + 1) * 8, 256);      // Shat (+ count channel)
+    b += align_up((size_t)2 * g.F * g.ny * (d + 1) * 8, 256);      // Nhat (worst case: all rows)
     return b;
 }
 
-int spec_update(const somb_map *m, const double *htab, const double *S, int d, const double *den, double scale,
-                const float *Wold, int j0, int j1, float *Wnew, double *num_out, void *ws, cudaStream_t st) {
+// den_mode: 0 = den given (direct, exact), 1 = compute den spectrally into `den`
+// with the zero threshold tau = hmin / 2.
+int spec_update(const somb_map *m, const double *htab, const double *S, const double *cnt, int d, double *den,
+                int den_mode, double tau, double scale, const float *Wold, int j0, int j1, float *Wnew,
+                double *num_out, void *ws, cudaStream_t st) {
     SpecGeom g = spec_geom(m);
     char *p = (char *)ws;
     auto take = [&](size_t bytes) { char *r = p; p += align_up(bytes, 256); return r; };
@@ -288,16 +316,20 @@ int spec_update(const somb_map *m, const double *htab, const double *S, int d, c
     double *sn = (double *)take((size_t)g.L * 8);
     const int nkeys = spec_nkeys(g);
     double *ktab = (double *)take((size_t)nkeys * 2 * g.F * 8);
-    double *Sh = (double *)take((size_t)2 * g.F * g.ny * d * 8);
+    const int Dp1 = d + 1;
+    double *Sh = (double *)take((size_t)2 * g.F * g.ny * Dp1 * 8);
     const int y0 = j0 / g.nx, y1 = (j1 + g.nx - 1) / g.nx, nyo = y1 - y0;
-    double *Nh = (double *)take((size_t)2 * g.F * nyo * d * 8);
+    double *Nh = (double *)take((size_t)2 * g.F * nyo * Dp1 * 8);
     spec_twiddle<<<(g.L + 255) / 256, 256, 0, st>>>(g.L, cs, sn);
     note_launch();
     spec_kernel_table<<<nkeys, 256, (size_t)g.L * 8, st>>>(g, htab, cs, sn, ktab);
     note_launch();
-    dgemm_launch(g.ny, 2 * g.F, d, g.nx, FwdA{g, cs, sn}, FwdB{g, S, d}, FwdEp{g, Sh, d}, st);
-    dgemm_launch(g.F, 2 * nyo, d, 2 * g.ny, MidA{g, ktab, y0, nyo}, MidB{g, Sh, d}, MidEp{g, Nh, nyo, d}, st);
-    dgemm_launch(nyo, g.nx, d, 2 * g.F, InvA{g, cs, sn}, InvB{g, Nh, nyo, d},
+    const int nc = den_mode ? Dp1 : d;     // channels carried through the DFTs
+    dgemm_launch(g.ny, 2 * g.F, nc, g.nx, FwdA{g, cs, sn}, FwdB{g, S, cnt, d}, FwdEp{g, Sh, Dp1}, st);
+    dgemm_launch(g.F, 2 * nyo, nc, 2 * g.ny, MidA{g, ktab, y0, nyo}, MidB{g, Sh, Dp1}, MidEp{g, Nh, nyo, Dp1}, st);
+    if (den_mode)
+        dgemm_launch(nyo, g.nx, 1, 2 * g.F, InvA{g, cs, sn}, DenB{g, Nh, nyo, Dp1}, DenEp{g, y0, j0, j1, tau, den}, st);
+    dgemm_launch(nyo, g.nx, d, 2 * g.F, InvA{g, cs, sn}, InvB{g, Nh, nyo, Dp1},
                  InvEp{g, y0, j0, j1, d, den, scale, 1.0 - scale, Wold, Wnew, num_out}, st);
     SOMB_LAUNCH_CHECK("spectral hood update");
     return SOMB_OK;

@@ -57,15 +57,18 @@ __global__ void data_stats_final(const double *__restrict__ psum, const float *_
 }
 
 // Xh = fp16((x - nu) * 2^xexp), xnorm = |x - nu|, x2 = |x|^2 (fp64).
+// Optional Xl = fp16 residual (v * 2^xexp - Xh): with it the screen runs the
+// 3-pass split product hi.hi + hi.lo + lo.hi (~22-bit operands).
 __global__ void data_pack_kernel(const float *__restrict__ X, int64_t n, int d,
                                  const float *__restrict__ nu, int xexp,
-                                 __half *__restrict__ Xh, int dp,
+                                 __half *__restrict__ Xh, __half *__restrict__ Xl, int dp,
                                  float *__restrict__ xnorm, double *__restrict__ x2) {
     int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     int lane = threadIdx.x & 31;
     if (row >= n) return;
     const float *x = X + row * d;
     __half *o = Xh + row * dp;
+    __half *ol = Xl ? Xl + row * dp : nullptr;
     double sc = ldexp(1.0, xexp);
     double nrm = 0.0, sq = 0.0;
     for (int k = lane; k < dp; k += 32) {
@@ -74,9 +77,12 @@ __global__ void data_pack_kernel(const float *__restrict__ X, int64_t n, int d,
             double v = xv - (double)nu[k];
             nrm += v * v;
             sq += xv * xv;
-            o[k] = __double2half(v * sc);
+            __half h = __double2half(v * sc);
+            o[k] = h;
+            if (ol) ol[k] = __double2half(v * sc - (double)__half2float(h));
         } else {
             o[k] = __double2half(0.0);
+            if (ol) ol[k] = __double2half(0.0);
         }
     }
     nrm = warp_sum(nrm);
@@ -146,7 +152,7 @@ __device__ __forceinline__ int pick_exp(float amax) {
 }
 
 __global__ void cb_pack(const float *__restrict__ W, int K, int d, const float *__restrict__ mu,
-                        int xexp, __half *__restrict__ Wh, int dp, int kp,
+                        int xexp, __half *__restrict__ Wh, __half *__restrict__ Wl, int dp, int kp,
                         float *__restrict__ c, const float *__restrict__ stats,
                         float *__restrict__ scal) {
     int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -154,13 +160,21 @@ __global__ void cb_pack(const float *__restrict__ W, int K, int d, const float *
     if (j >= kp) return;
     int sexp = pick_exp(stats[1]);
     __half *o = Wh + (int64_t)j * dp;
+    __half *ol = Wl ? Wl + (int64_t)j * dp : nullptr;
     if (j < K) {
         const float *w = W + (int64_t)j * d;
         double sc = ldexp(1.0, sexp);
-        for (int k = lane; k < dp; k += 32)
-            o[k] = __double2half(k < d ? ((double)w[k] - (double)mu[k]) * sc : 0.0);
+        for (int k = lane; k < dp; k += 32) {
+            double v = k < d ? ((double)w[k] - (double)mu[k]) * sc : 0.0;
+            __half h = __double2half(v);
+            o[k] = h;
+            if (ol) ol[k] = __double2half(v - (double)__half2float(h));
+        }
     } else {
-        for (int k = lane; k < dp; k += 32) o[k] = __double2half(0.0);
+        for (int k = lane; k < dp; k += 32) {
+            o[k] = __double2half(0.0);
+            if (ol) ol[k] = __double2half(0.0);
+        }
         if (lane == 0) c[j] = INFINITY;
     }
     if (j == 0 && lane == 0) {
@@ -198,13 +212,13 @@ extern "C" int somb_data_stats(const float *X, int64_t n, int32_t d, float *nu, 
 }
 
 extern "C" int somb_data_pack(const float *X, int64_t n, int32_t d, const float *nu, int32_t xexp,
-                              uint16_t *Xh, int32_t dp, float *xnorm, double *x2, void *stream) {
+                              uint16_t *Xh, uint16_t *Xl, int32_t dp, float *xnorm, double *x2, void *stream) {
     SOMB_REQUIRE(d > 0 && dp >= d && dp % 8 == 0, SOMB_E_INPUT, "data_pack: bad pitch d=%d dp=%d", d, dp);
     if (n == 0) return SOMB_OK;
     int rows_per_block = 8;
     int64_t blocks = (n + rows_per_block - 1) / rows_per_block;
     data_pack_kernel<<<(unsigned)blocks, 32 * rows_per_block, 0, as_stream(stream)>>>(
-        X, n, d, nu, xexp, (__half *)Xh, dp, xnorm, x2);
+        X, n, d, nu, xexp, (__half *)Xh, (__half *)Xl, dp, xnorm, x2);
     note_launch();
     SOMB_LAUNCH_CHECK("somb_data_pack");
     return SOMB_OK;
@@ -216,7 +230,7 @@ extern "C" size_t somb_codebook_ws(int32_t K, int32_t d) {
 }
 
 extern "C" int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const float *nu,
-                                     int32_t xexp, uint16_t *Wh, int32_t dp, int32_t kp, float *c,
+                                     int32_t xexp, uint16_t *Wh, uint16_t *Wl, int32_t dp, int32_t kp, float *c,
                                      double *w2, float *scal, void *ws, void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && dp % 8 == 0 && kp >= K && kp % 256 == 0,
                  SOMB_E_INPUT, "codebook_prepare: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
@@ -231,7 +245,7 @@ extern "C" int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const
     note_launch();
     cb_rowstats<<<(K + 7) / 8, 256, 0, st>>>(W, K, d, mu, mu_nu, c, w2, nrm, stats);
     note_launch();
-    cb_pack<<<(kp + 7) / 8, 256, 0, st>>>(W, K, d, mu, xexp, (__half *)Wh, dp, kp, c, stats, scal);
+    cb_pack<<<(kp + 7) / 8, 256, 0, st>>>(W, K, d, mu, xexp, (__half *)Wh, (__half *)Wl, dp, kp, c, stats, scal);
     note_launch();
     SOMB_LAUNCH_CHECK("somb_codebook_prepare");
     return SOMB_OK;

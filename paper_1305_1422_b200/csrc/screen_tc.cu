@@ -41,13 +41,17 @@ constexpr int TC_HALF_CAP = SOMB_CAND_CAP / 2;   // candidates per (row, column 
 constexpr int TC_ROWS = 128;                      // data rows per CTA (TMEM lanes)
 constexpr uint32_t TC_CAND_BYTES = TC_EPI_WARPS * 32 * TC_HALF_CAP * 8;
 
-template <int CG>
+// PASSES = 1: fp16 operands; PASSES = 3: split operands (hi + lo residual),
+// D += hi.hi + hi.lo + lo.hi (~22-bit operand precision, 3x the MMAs) for
+// small feature counts where the 1-pass fp16 window holds too many
+// near-tied nodes.  A stage holds [A_hi | B_hi | A_lo | B_lo].
+template <int CG, int PASSES = 1>
 struct TcCfg {
     static constexpr int B_ROWS = TC_BN / CG;                      // codebook rows loaded per CTA
     static constexpr uint32_t A_BYTES = TC_ROWS * TC_BK * 2;       // 16 KB
     static constexpr uint32_t B_BYTES = B_ROWS * TC_BK * 2;        // 32 KB (CG 1) / 16 KB (CG 2)
-    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = CG == 2 ? 6 : 4;
+    static constexpr uint32_t STAGE_BYTES = (PASSES == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
+    static constexpr int STAGES = 192 * 1024 / STAGE_BYTES;   // 6 / 4 (1-pass), 3 / 2 (3-pass)
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + TC_CAND_BYTES + 1024 + 256;
     // kind::f16 instruction descriptor: A,B = f16, D = f32, K-major, M = 128 CG, N = 256
     static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((128 * CG) >> 4) << 24);
@@ -208,19 +212,19 @@ __constant__ int g_profile_mode = 0;
 __constant__ int g_a_evict_last = 0;
 
 // ------------------------------------------------------------------ kernel
-template <int CG>
-__device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const CUtensorMap *map_w, int64_t n,
+template <int CG, int PASSES>
+__device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const CUtensorMap *map_w,
+                                               const CUtensorMap *map_xl, const CUtensorMap *map_wl, int64_t n,
                                                int dp, int kp, const float *__restrict__ c,
                                                const float *__restrict__ xnorm, const float *__restrict__ scal,
                                                float wcoef, const float *__restrict__ thr0, int *__restrict__ cand,
                                                int *__restrict__ ccount, int *__restrict__ flags,
                                                float *__restrict__ dump) {
-    using Cfg = TcCfg<CG>;
+    using Cfg = TcCfg<CG, PASSES>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t *sA = smem;                                     // [stage][A_BYTES]
-    uint8_t *sB = smem + S * Cfg::A_BYTES;                  // [stage][B_BYTES]
+    // stage s: A_hi at smem + s*STAGE_BYTES, B_hi after it, then A_lo, B_lo (3-pass)
     float *cbv = (float *)(smem + S * Cfg::STAGE_BYTES);
     int *cbi = (int *)(cbv + TC_EPI_WARPS * 32 * TC_HALF_CAP);
     uint64_t *bars = (uint64_t *)(smem + S * Cfg::STAGE_BYTES + TC_CAND_BYTES);
@@ -282,11 +286,17 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         mbar_wait(empty0 + 8 * stage, phase ^ 1);
                         const uint32_t fb = full0 + 8 * stage;
                         if (leader) mbar_expect_tx(fb, CG * Cfg::STAGE_BYTES);
+                        uint8_t *st0 = smem + stage * Cfg::STAGE_BYTES;
                         if (hint_a)
-                            tma_load_2d_hint<CG>(smem_u32(sA + stage * Cfg::A_BYTES), map_x, fb, kb * TC_BK, row0, pol_a);
+                            tma_load_2d_hint<CG>(smem_u32(st0), map_x, fb, kb * TC_BK, row0, pol_a);
                         else
-                            tma_load_2d<CG>(smem_u32(sA + stage * Cfg::A_BYTES), map_x, fb, kb * TC_BK, row0);
-                        tma_load_2d<CG>(smem_u32(sB + stage * Cfg::B_BYTES), map_w, fb, kb * TC_BK, node0);
+                            tma_load_2d<CG>(smem_u32(st0), map_x, fb, kb * TC_BK, row0);
+                        tma_load_2d<CG>(smem_u32(st0 + Cfg::A_BYTES), map_w, fb, kb * TC_BK, node0);
+                        if constexpr (PASSES == 3) {
+                            tma_load_2d<CG>(smem_u32(st0 + Cfg::A_BYTES + Cfg::B_BYTES), map_xl, fb, kb * TC_BK, row0);
+                            tma_load_2d<CG>(smem_u32(st0 + 2 * Cfg::A_BYTES + Cfg::B_BYTES), map_wl, fb, kb * TC_BK,
+                                            node0);
+                        }
                         if (++stage == S) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -306,12 +316,17 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     for (int kb = 0; kb < KB; ++kb) {
                         mbar_wait(full0 + 8 * stage, phase);
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
-                        const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+                        const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                        const uint32_t b0 = a0 + Cfg::A_BYTES;
 #pragma unroll
                         for (int k = 0; k < TC_BK / TC_UMMA_K; ++k) {
                             tc_mma_f16<CG>(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), Cfg::IDESC,
                                            (kb | k) != 0);
+                            if constexpr (PASSES == 3) {
+                                const uint32_t al = b0 + Cfg::B_BYTES, bl = al + Cfg::A_BYTES;
+                                tc_mma_f16<CG>(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(bl + 32 * k), Cfg::IDESC, 1);
+                                tc_mma_f16<CG>(d_tmem, sw128_desc(al + 32 * k), sw128_desc(b0 + 32 * k), Cfg::IDESC, 1);
+                            }
                         }
                         tc_commit<CG>(empty0 + 8 * stage);   // frees the smem slot(s) when these MMAs retire
                         if (++stage == S) { stage = 0; phase ^= 1; }
@@ -419,17 +434,22 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
 }
 
 #define SCREEN_TC_ARGS                                                                                              \
-    const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, int64_t n, int dp, int kp, \
+    const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,                           \
+        const __grid_constant__ CUtensorMap map_xl, const __grid_constant__ CUtensorMap map_wl, int64_t n, int dp, int kp, \
         const float *__restrict__ c, const float *__restrict__ xnorm, const float *__restrict__ scal, float wcoef,  \
         const float *__restrict__ thr0, int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags,  \
         float *__restrict__ dump
 
+template <int P>
 __global__ void __launch_bounds__(TC_THREADS, 1) screen_tc1_kernel(SCREEN_TC_ARGS) {
-    screen_tc_body<1>(&map_x, &map_w, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount, flags, dump);
+    screen_tc_body<1, P>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount, flags,
+                         dump);
 }
 
+template <int P>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) screen_tc2_kernel(SCREEN_TC_ARGS) {
-    screen_tc_body<2>(&map_x, &map_w, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount, flags, dump);
+    screen_tc_body<2, P>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount, flags,
+                         dump);
 }
 
 // --------------------------------------------------------------- host side
@@ -465,8 +485,14 @@ static int make_map(CUtensorMap *map, const void *base, uint64_t inner, uint64_t
 
 static int g_tc_group = 2;   // SOMB_TC_GROUP=1 selects the single-CTA variant (A/B testing)
 
-int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int kp, const float *c,
-                     const float *xnorm, const float *scal, float wcoef, const float *thr0, int *cand,
+template <class KernelT>
+static int set_smem(KernelT k, uint32_t bytes, const char *what) {
+    cudaError_t r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    return r == cudaSuccess ? SOMB_OK : cuda_status(r, what);
+}
+
+int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh, const __half *Wl, int kp,
+                     const float *c, const float *xnorm, const float *scal, float wcoef, const float *thr0, int *cand,
                      int *ccount, int *flags, float *dump, cudaStream_t st) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % TC_BN == 0, SOMB_E_INPUT, "screen_tc: dp %% 8 and kp %% 256 required");
     static bool init = false;
@@ -479,19 +505,20 @@ int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int 
         const char *ae = getenv("SOMB_A_EVICT_LAST");
         int a_last = ae ? atoi(ae) : 0;
         cudaMemcpyToSymbol(g_a_evict_last, &a_last, sizeof(int));
-        cudaError_t r1 = cudaFuncSetAttribute(screen_tc1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              TcCfg<1>::SMEM);
-        cudaError_t r2 = cudaFuncSetAttribute(screen_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              TcCfg<2>::SMEM);
-        if (r1 != cudaSuccess) return cuda_status(r1, "screen_tc1 smem attribute");
-        if (r2 != cudaSuccess) return cuda_status(r2, "screen_tc2 smem attribute");
+        int rc = set_smem(screen_tc1_kernel<1>, TcCfg<1, 1>::SMEM, "screen_tc1 smem");
+        if (!rc) rc = set_smem(screen_tc2_kernel<1>, TcCfg<2, 1>::SMEM, "screen_tc2 smem");
+        if (!rc) rc = set_smem(screen_tc1_kernel<3>, TcCfg<1, 3>::SMEM, "screen_tc1x3 smem");
+        if (!rc) rc = set_smem(screen_tc2_kernel<3>, TcCfg<2, 3>::SMEM, "screen_tc2x3 smem");
+        if (rc) return rc;
         init = true;
     }
     const int cg = g_tc_group;
-    CUtensorMap mx, mw;
+    const bool three = Xl != nullptr && Wl != nullptr;
+    CUtensorMap mx, mw, mxl, mwl;
     int rc = make_map(&mx, Xh, (uint64_t)dp, (uint64_t)n, TC_ROWS);
-    if (rc) return rc;
-    rc = make_map(&mw, Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg));
+    if (!rc) rc = make_map(&mw, Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg));
+    if (!rc) rc = make_map(&mxl, three ? Xl : Xh, (uint64_t)dp, (uint64_t)n, TC_ROWS);
+    if (!rc) rc = make_map(&mwl, three ? Wl : Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg));
     if (rc) return rc;
     int dev = 0, sms = kSmCount;
     cudaGetDevice(&dev);
@@ -501,12 +528,15 @@ int launch_screen_tc(const __half *Xh, int64_t n, int dp, const __half *Wh, int 
     const int units = (int)((n + TC_ROWS * cg - 1) / (TC_ROWS * cg));
     const int max_units = sms / cg;
     const int grid = cg * (units < max_units ? units : max_units);
-    if (cg == 2)
-        screen_tc2_kernel<<<grid, TC_THREADS, TcCfg<2>::SMEM, st>>>(mx, mw, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand,
-                                                                     ccount, flags, dump);
-    else
-        screen_tc1_kernel<<<grid, TC_THREADS, TcCfg<1>::SMEM, st>>>(mx, mw, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand,
-                                                                     ccount, flags, dump);
+#define SCREEN_LAUNCH(KERN, CGV, PV)                                                                                  \
+    KERN<PV><<<grid, TC_THREADS, TcCfg<CGV, PV>::SMEM, st>>>(mx, mw, mxl, mwl, n, dp, kp, c, xnorm, scal, wcoef, thr0, \
+                                                             cand, ccount, flags, dump)
+    if (cg == 2) {
+        if (three) SCREEN_LAUNCH(screen_tc2_kernel, 2, 3); else SCREEN_LAUNCH(screen_tc2_kernel, 2, 1);
+    } else {
+        if (three) SCREEN_LAUNCH(screen_tc1_kernel, 1, 3); else SCREEN_LAUNCH(screen_tc1_kernel, 1, 1);
+    }
+#undef SCREEN_LAUNCH
     note_launch();
     SOMB_LAUNCH_CHECK("screen_tc");
     return SOMB_OK;

@@ -26,6 +26,11 @@ from .grid import GridType, MapType, Neighborhood, distance_table
 
 _DEF_WINDOW_KAPPA = 16.0   # screening window = kappa * u16 * |x-nu| * max|delta| / sqrt(D); measured max screen error <= 6.1 units (tools/calib_screen.py), so the window covers 2x that with 30% margin
 _U16 = 2.0 ** -11
+# 3-pass split screen (hi.hi + hi.lo + lo.hi): its error is dominated by fp32
+# accumulation, measured max ~ D/8192 in the same units (tools/calib_screen.py:
+# 0.01 / 0.03 / 0.09 at D = 128 / 256 / 1000); the window is 2.6x that + 0.02.
+def _kappa3(d: int) -> float:
+    return 2.6 * d / 8192.0 + 0.02
 
 
 @dataclass
@@ -34,6 +39,8 @@ class EngineOptions:
     window_kappa: float = _DEF_WINDOW_KAPPA
     hypot_table: bool = True          # numpy-hypot distances for rect grids (bit parity)
     seed_prev: bool = True            # seed the screen threshold from the previous BMUs
+    screen_passes: int = 0            # 0 auto (3 if the padded feature count <= 256), 1, or 3
+    window_kappa3: Optional[float] = None     # None: _kappa3(d)
     conv: str = "auto"                # neighbourhood convolution: "auto", "direct", "spectral"
 
 
@@ -88,7 +95,11 @@ class SomEngine:
                                  _lib.GRID_HEX if grid is GridType.HEXAGONAL else _lib.GRID_RECT,
                                  _lib.TOROID if map_type is MapType.TOROID else _lib.PLANAR)
         x = data.values if isinstance(data, DenseDataset) else data
-        self._upload_dense(x)
+        self._upload_dense(x, dry=True)
+        dp0 = _round_up(self.d, 8)
+        p = self.opt.screen_passes
+        self.passes = 3 if (p == 3 or (p == 0 and dp0 <= 256)) and self.opt.screen == "tensor" else 1
+        self.pack_dataset()
         d = self.d
         self.dp = _round_up(d, 8)
         self.kp = _round_up(self.K, 256)
@@ -101,6 +112,8 @@ class SomEngine:
         self.W = torch.zeros((self.kpad, d), dtype=f32, device=dev)
         self.W2 = torch.zeros((self.kpad, d), dtype=f32, device=dev)
         self.Wh = torch.empty((self.kp, self.dp), dtype=torch.float16, device=dev)
+        self.Wl = (torch.empty((self.kp, self.dp), dtype=torch.float16, device=dev)
+                   if self.passes == 3 else None)
         self.c = torch.empty(self.kp, dtype=f32, device=dev)
         self.w2 = torch.empty(self.K, dtype=f64, device=dev)
         self.scal = torch.empty(4, dtype=f32, device=dev)
@@ -121,12 +134,16 @@ class SomEngine:
                  lib.somb_node_sums_ws(n, d, self.K),
                  lib.somb_hood_ws(C.byref(self.cmap), self.K, d), 1 << 16)
         self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)
-        self.window_coef = float(self.opt.window_kappa * _U16 / math.sqrt(d))
+        if self.passes == 3:
+            kappa = self.opt.window_kappa3 if self.opt.window_kappa3 is not None else _kappa3(d)
+        else:
+            kappa = self.opt.window_kappa
+        self.window_coef = float(kappa * _U16 / math.sqrt(d))
         self.screen_impl = {"tensor": 0, "simt": 1, "exact": 2}[self.opt.screen]
         self.has_prev = False
 
     # ------------------------------------------------------------ dataset
-    def _upload_dense(self, x):
+    def _upload_dense(self, x, dry=False):
         if _is_torch(x):
             xt = x.to(self.dev, dtype=torch.float32, non_blocking=True).contiguous()
         else:
@@ -136,7 +153,8 @@ class SomEngine:
             xt = xh.to(self.dev, non_blocking=True)
         self.X = xt
         self.n, self.d = int(xt.shape[0]), int(xt.shape[1])
-        self.pack_dataset()
+        if not dry:
+            self.pack_dataset()
 
     def pack_dataset(self):
         """Centre + fp16 copy of the resident rows (once per dataset)."""
@@ -150,10 +168,12 @@ class SomEngine:
         a = float(absmax.item())                 # one host sync per dataset
         self.xexp = 0 if a <= 0.0 or not math.isfinite(a) else 14 - math.frexp(a)[1]
         self.Xh = torch.empty((max(n, 1), self.dp), dtype=torch.float16, device=dev)
+        self.Xl = (torch.empty((max(n, 1), self.dp), dtype=torch.float16, device=dev)
+                   if getattr(self, "passes", 1) == 3 else None)
         self.xnorm = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         self.x2 = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
         _lib.call("somb_data_pack", _ptr(self.X), n, d, _ptr(self.nu), self.xexp, _ptr(self.Xh),
-                  self.dp, _ptr(self.xnorm), _ptr(self.x2), st)
+                  _ptr(self.Xl), self.dp, _ptr(self.xnorm), _ptr(self.x2), st)
 
     # ----------------------------------------------------------- codebook
     def set_codebook(self, w):
@@ -168,8 +188,8 @@ class SomEngine:
     # ------------------------------------------------------------- phases
     def prepare(self):
         _lib.call("somb_codebook_prepare", _ptr(self.W), self.K, self.d, _ptr(self.nu), self.xexp,
-                  _ptr(self.Wh), self.dp, self.kp, _ptr(self.c), _ptr(self.w2), _ptr(self.scal),
-                  _ptr(self.ws), _stream(self.dev))
+                  _ptr(self.Wh), _ptr(self.Wl), self.dp, self.kp, _ptr(self.c), _ptr(self.w2),
+                  _ptr(self.scal), _ptr(self.ws), _stream(self.dev))
 
     # optional per-phase CUDA-event timing (bench.py): name -> [(start, end), ...]
     timing = None
@@ -194,8 +214,9 @@ class SomEngine:
         st = _stream(self.dev)
         self._mark("screen", True)
         prev = self.bmu if (self.has_prev and self.opt.seed_prev) else None
-        _lib.call("somb_bmu_screen", _ptr(self.Xh), _ptr(self.xnorm), self.n, self.dp, _ptr(self.Wh),
-                  _ptr(self.c), self.K, self.kp, _ptr(self.scal), C.c_float(self.window_coef),
+        _lib.call("somb_bmu_screen", _ptr(self.Xh), _ptr(self.Xl), _ptr(self.xnorm), self.n, self.dp,
+                  _ptr(self.Wh), _ptr(self.Wl), _ptr(self.c), self.K, self.kp, _ptr(self.scal),
+                  C.c_float(self.window_coef),
                   _ptr(prev), self.screen_impl, _ptr(self.flags), _ptr(self.ws), st)
         self._mark("screen", False)
         self._mark("rerank", True)
@@ -210,8 +231,9 @@ class SomEngine:
         self.prepare()
         m = min(self.n, 128)
         dump = torch.full((m, self.kp), float("nan"), dtype=torch.float32, device=self.dev)
-        _lib.call("somb_debug_screen_dump", _ptr(self.Xh), _ptr(self.xnorm), self.n, self.dp,
-                  _ptr(self.Wh), _ptr(self.c), self.kp, _ptr(self.scal), C.c_float(self.window_coef),
+        _lib.call("somb_debug_screen_dump", _ptr(self.Xh), _ptr(self.Xl), _ptr(self.xnorm), self.n,
+                  self.dp, _ptr(self.Wh), _ptr(self.Wl), _ptr(self.c), self.kp, _ptr(self.scal),
+                  C.c_float(self.window_coef),
                   _ptr(dump), _ptr(self.ws), _stream(self.dev))
         return dump[:, : self.K]
 

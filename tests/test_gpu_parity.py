@@ -157,6 +157,7 @@ def test_spectral_conv_large_map(mt, grid):
     nx, ny, d = 64, 40, 37
     k = nx * ny
     c = rng.integers(0, 6, k).astype(np.float64)
+    c[: k // 2] = 0                       # empty half-map: exact den zeros at small radius
     s = rng.random((k, d)) * c[:, None]
     w = rng.random((k, d), dtype=np.float32)
     eng = S.SomEngine(S.DenseDataset(rng.random((4, d), dtype=np.float32)), nx, ny, S.MapType(mt),
@@ -170,7 +171,9 @@ def test_spectral_conv_large_map(mt, grid):
         eng.update(radius, 0.5, 1e-3, num_out=num, den_out=den, all_nodes=True)
         wn, wd = O.conv_update(s, c, nx, ny, radius, 1e-3, mt, grid)
         np.testing.assert_allclose(num.cpu().numpy(), wn, rtol=1e-11, atol=1e-13 * np.abs(wn).max())
-        assert np.array_equal(den.cpu().numpy(), wd) or np.allclose(den.cpu().numpy(), wd, rtol=1e-13)
+        gd = den.cpu().numpy()
+        assert np.array_equal(gd > 0, wd > 0)               # exact zero pattern (blend mask)
+        np.testing.assert_allclose(gd, wd, rtol=1e-9, atol=0)
         np.testing.assert_allclose(eng.codebook(), O.blend(w, wn, wd, 0.5), rtol=2e-7)
 
 

@@ -17,11 +17,14 @@ nx = int(sys.argv[3]) if len(sys.argv) > 3 else 200
 ny = int(sys.argv[4]) if len(sys.argv) > 4 else 200
 E = int(sys.argv[5]) if len(sys.argv) > 5 else 6
 tor = (sys.argv[6] != "0") if len(sys.argv) > 6 else True
+passes = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 g = torch.Generator(device="cuda")
 g.manual_seed(1001)
 X = torch.rand((n, d), generator=g, device="cuda")
 mt = S.MapType.TOROID if tor else S.MapType.PLANAR
-eng = SomEngine(X, nx, ny, mt)
+from paper_1305_1422_b200.engine import EngineOptions  # noqa: E402
+eng = SomEngine(X, nx, ny, mt, options=EngineOptions(screen_passes=passes))
+print("passes", eng.passes, "window kappa", eng.window_coef * math.sqrt(d) / 2.0 ** -11)
 cfg = S.resolve_defaults(S.TrainConfig(n_epochs=10, n_columns=nx, n_rows=ny, map_type=mt))
 eng.set_codebook(S.init_codebook(cfg, d).weights)
 x64 = X[:128].double()
@@ -44,7 +47,7 @@ for e in range(E):
     rmin = r.min(1, keepdim=True).values
     out = [f"ep{e} r={st.radius:.1f}: max|err|/(u16 |x'| nmax/sqrt(D)) = {ratio:.2f}; "
            f"exact-argmin screen rank max {int(rank.max())}"]
-    for kappa in (4, 8, 12, 16, 24):
+    for kappa in ((0.05, 0.1, 0.25, 0.5, 1.0) if eng.passes == 3 else (4, 8, 12, 16, 24)):
         w = kappa * scale[:, :1]
         cnt = (r <= rmin + w).sum(1).float()
         out.append(f"k{kappa}: mean {cnt.mean():.1f} max {int(cnt.max())}")
