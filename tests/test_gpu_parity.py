@@ -243,3 +243,57 @@ def test_cfg1_bit_exact_tensor_screen():
     mism = np.sum(cb.weights != g["cfg1_w"])
     assert mism <= cb.weights.size * 1e-4, f"{mism} codebook entries differ"
     assert np.array_equal(bmus, g["cfg1_bmus"])
+
+
+@pytest.mark.parametrize("grid,nbh,compact,mt", [
+    ("hexagonal", "gaussian", False, "toroid"),
+    ("hexagonal", "bubble", True, "toroid"),      # cfg4 semantics
+    ("hexagonal", "gaussian", True, "planar"),
+    ("rectangular", "bubble", False, "planar"),
+    ("rectangular", "gaussian", True, "toroid"),
+])
+@pytest.mark.parametrize("screen", ["tensor", "exact"])
+def test_train_extensions_vs_oracle(grid, nbh, compact, mt, screen):
+    """Hex / bubble / compact-support training end to end against the oracle's
+    restatement (builder definitions), on well-separated clusters."""
+    rng = np.random.default_rng(12)
+    cen = rng.random((6, 12)) * 4
+    x = np.concatenate([c + 0.05 * rng.standard_normal((150, 12)) for c in cen]).astype(np.float32)
+    nx, ny = 12, 8
+    cfg = S.TrainConfig(n_epochs=6, n_columns=nx, n_rows=ny, map_type=S.MapType(mt),
+                        kernel=S.Kernel.DENSE_BLOCKED, grid=S.GridType(grid),
+                        neighborhood=S.Neighborhood(nbh), compact_support=compact, seed=5)
+    cb, bmus, u = S.train(S.DenseDataset(x), cfg, options=_opts(screen))
+    og = O.HEX if grid == "hexagonal" else O.RECT
+    w, bm, uo, _ = O.train(x, nx, ny, n_epochs=6, map_type=mt, seed=5, grid=og, neighborhood=nbh,
+                           compact=compact)
+    assert rel_err(cb.weights, w) <= REL_TOL
+    assert rel_err(u.heights, uo) <= REL_TOL
+    fb = bmus[:, 0].astype(np.int64) * nx + bmus[:, 1]
+    ob = bm[:, 0].astype(np.int64) * nx + bm[:, 1]
+    assert_bmus_tie_aware(fb, ob, x, w)
+
+
+def test_cfg2_shape_teacher_forced_epochs():
+    """Full cfg2 map (200x200 toroid, d=1000, spectral update, tcgen05 screen)
+    on a 4096-row slice: each epoch's device result is compared with the
+    oracle epoch fed the SAME entering codebook (teacher forcing)."""
+    rng = np.random.default_rng(1001)
+    x = rng.random((4096, 1000), dtype=np.float32)
+    nx = ny = 200
+    cfg = S.resolve_defaults(S.TrainConfig(n_epochs=10, n_columns=nx, n_rows=ny,
+                                           map_type=S.MapType.TOROID, kernel=S.Kernel.DENSE_BLOCKED))
+    w = S.init_codebook(cfg, 1000).weights
+    eng = S.SomEngine(S.DenseDataset(x), nx, ny, S.MapType.TOROID)
+    for e in (0, 1, 5):
+        st = S.epoch_schedules(cfg, e)
+        eng.set_codebook(w)
+        eng.epoch(st.radius, st.scale, cfg.influence_cutoff)
+        got = eng.codebook()
+        bmu_g = eng.bmu[:4096].cpu().numpy()
+        ob, _, num, den = O.search_accumulate(x, w, nx, ny, st.radius, cfg.influence_cutoff, O.TOROID,
+                                              workers=8)
+        want = O.blend(w, num, den, st.scale)
+        assert_bmus_tie_aware(bmu_g, ob, x, w)
+        assert rel_err(got, want) <= 1e-6, e
+        w = want
