@@ -181,6 +181,28 @@ SOMB_API int somb_hood_update(const double *S, const double *cnt, int32_t d,
 SOMB_API int somb_blend(const float *W_old, const double *num, const double *den,
                int32_t K, int32_t d, double scale, float *W_new, void *stream);
 
+/* ---- sparse (CSR) rows: kernels.py:208-222, 229-242, 315-321 ---------
+ * Row stats: x2[i] = sum v^2 (fp64, nnz order), xnorm = sqrt(x2), nnz_max. */
+SOMB_API int somb_sparse_row_stats(const int64_t *rowptr, const float *val, int64_t n,
+                                   double *x2, float *xnorm, int32_t *nnz_max, void *stream);
+/* dT[k][j] = fp32(w_jk - mu_k) (pitch kp, zero padding); mu = the codebook
+ * mean written by somb_codebook_prepare into the first d floats of its ws. */
+SOMB_API int somb_sparse_codebook_T(const float *W, const float *mu, int32_t K, int32_t d,
+                                    int32_t kp, float *dT, void *stream);
+/* fp32 gather screen over dT + exact fp64 sparse re-rank (exact = 1: scan
+ * every node, no screen).  ws >= somb_bmu_ws(n). */
+SOMB_API int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const float *val,
+                             int64_t n, int32_t d, const float *dT, const float *W,
+                             const float *c, const double *w2, int32_t K, int32_t kp,
+                             const float *scal, const double *x2, const float *xnorm,
+                             float window_coef, int32_t exact, int32_t *bmu,
+                             double *d2min, int32_t *flags, void *ws, void *stream);
+/* S (K x d, fp64, dense) / cnt from CSR rows; ws >= somb_node_sums_ws(n, 1, K). */
+SOMB_API int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col,
+                                   const float *val, int64_t n, int32_t d,
+                                   const int32_t *bmu, int32_t K, double *S,
+                                   double *cnt, void *ws, void *stream);
+
 /* Number of kernels this library has launched (process lifetime). */
 SOMB_API unsigned long long somb_launch_count(void);
 

@@ -64,6 +64,11 @@ SIGNATURES = {
     "somb_hood_update": (C.c_int, [P, P, I32, C.POINTER(SombMap), C.POINTER(SombHood), F64, P,
                                    P, I32, I32, P, P, P, P, P]),
     "somb_blend": (C.c_int, [P, P, P, I32, I32, F64, P, P]),
+    "somb_sparse_row_stats": (C.c_int, [P, P, I64, P, P, P, P]),
+    "somb_sparse_codebook_T": (C.c_int, [P, P, I32, I32, I32, P, P]),
+    "somb_bmu_sparse": (C.c_int, [P, P, P, I64, I32, P, P, P, P, I32, I32, P, P, P, F32, I32,
+                                  P, P, P, P, P]),
+    "somb_node_sums_sparse": (C.c_int, [P, P, P, I64, I32, P, I32, P, P, P, P]),
     "somb_umatrix": (C.c_int, [P, I32, C.POINTER(SombMap), P, P]),
 }
 

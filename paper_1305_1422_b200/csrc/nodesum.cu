@@ -231,20 +231,22 @@ extern "C" size_t somb_node_sums_ws(int64_t n, int32_t d, int32_t K) {
     return b + 256;
 }
 
-extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const int32_t *bmu, int32_t K,
-                                    double *S, double *cnt, void *ws, void *stream) {
-    SOMB_REQUIRE(K > 0 && d > 0 && n >= 0 && n < (1ll << 31), SOMB_E_INPUT,
-                 "node_sums: bad shape n=%lld d=%d K=%d", (long long)n, d, K);
-    cudaStream_t st = as_stream(stream);
-    NodeSumWs w = carve(ws, n, d, K);
-    cudaMemsetAsync(S, 0, (size_t)K * d * sizeof(double), st);
+namespace somb {
+// Stable grouping of rows by BMU: perm = rows sorted by (bmu, row), off =
+// bucket offsets (K + 1), cnt = bucket sizes as fp64.  Shared by the dense and
+// sparse node sums.  ws is carved like somb_node_sums_ws.
+int node_bucket_sort(const int *bmu, int64_t n, int K, void *ws, const int **perm_out, const int **off_out,
+                     double *cnt, cudaStream_t st) {
+    NodeSumWs w = carve(ws, n, 1, K);
     cudaMemsetAsync(w.cnt, 0, (size_t)(K + 1) * sizeof(int), st);
+    *off_out = w.off;
     if (n == 0) {
         cudaMemsetAsync(cnt, 0, (size_t)K * sizeof(double), st);
-        SOMB_LAUNCH_CHECK("node_sums(empty)");
+        cudaMemsetAsync(w.off, 0, (size_t)(K + 1) * sizeof(int), st);
+        *perm_out = w.vA;
+        SOMB_LAUNCH_CHECK("node_bucket_sort(empty)");
         return SOMB_OK;
     }
-    // --- stable sort of (bmu, row) by bmu
     int bits = 0;
     while ((1 << bits) < K) ++bits;
     int passes = (bits + 7) / 8;
@@ -252,48 +254,52 @@ extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const 
     const int *kin = bmu;
     const int *vin = nullptr;
     int *kout = w.kA, *vout = w.vA;
+    if (passes == 0) passes = 1;   // K == 1: one identity pass (all digits 0)
     for (int p = 0; p < passes; ++p) {
         radix_hist<<<ntiles, kSortThreads, 0, st>>>(kin, n, 8 * p, ntiles, w.hist);
         note_launch();
         exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.hist, 256 * ntiles, w.hsc);
         note_launch();
-        radix_scatter<<<ntiles, kSortThreads, 0, st>>>(kin, vin, n, 8 * p, ntiles, w.hsc, kout, vout,
-                                                       p == 0);
+        radix_scatter<<<ntiles, kSortThreads, 0, st>>>(kin, vin, n, 8 * p, ntiles, w.hsc, kout, vout, p == 0);
         note_launch();
         kin = kout;
         vin = vout;
         kout = (kout == w.kA) ? w.kB : w.kA;
         vout = (vout == w.vA) ? w.vB : w.vA;
     }
-    const int *perm = vin;
-    if (passes == 0) {   // K == 1: every row in node 0, identity order
-        // reuse the scatter kernel as an iota copy with a 0-bit digit
-        radix_hist<<<ntiles, kSortThreads, 0, st>>>(bmu, n, 0, ntiles, w.hist);
-        note_launch();
-        exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.hist, 256 * ntiles, w.hsc);
-        note_launch();
-        radix_scatter<<<ntiles, kSortThreads, 0, st>>>(bmu, nullptr, n, 0, ntiles, w.hsc, w.kA, w.vA, 1);
-        note_launch();
-        perm = w.vA;
-    }
-    // --- bucket offsets and segment plan
+    *perm_out = vin;
     bucket_count<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bmu, n, w.cnt);
     note_launch();
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.cnt, K, w.off);
     note_launch();
     seg_plan<<<(K + 255) / 256, 256, 0, st>>>(w.cnt, K, w.nseg, w.mseg, cnt);
     note_launch();
+    SOMB_LAUNCH_CHECK("node_bucket_sort");
+    return SOMB_OK;
+}
+}  // namespace somb
+
+extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const int32_t *bmu, int32_t K,
+                                    double *S, double *cnt, void *ws, void *stream) {
+    SOMB_REQUIRE(K > 0 && d > 0 && n >= 0 && n < (1ll << 31), SOMB_E_INPUT,
+                 "node_sums: bad shape n=%lld d=%d K=%d", (long long)n, d, K);
+    cudaStream_t st = as_stream(stream);
+    NodeSumWs w = carve(ws, n, d, K);
+    cudaMemsetAsync(S, 0, (size_t)K * d * sizeof(double), st);
+    const int *perm = nullptr, *off = nullptr;
+    int rc = node_bucket_sort(bmu, n, K, ws, &perm, &off, cnt, st);
+    if (rc || n == 0) return rc;
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.nseg, K, w.segoff);
     note_launch();
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.mseg, K, w.msegoff);
     note_launch();
     unsigned maxseg = (unsigned)(K + (n + kSeg - 1) / kSeg);
     if (d <= 128)
-        seg_sum<1><<<maxseg, 128, 0, st>>>(X, d, perm, w.off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
+        seg_sum<1><<<maxseg, 128, 0, st>>>(X, d, perm, off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
     else if (d <= 512)
-        seg_sum<4><<<maxseg, 128, 0, st>>>(X, d, perm, w.off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
+        seg_sum<4><<<maxseg, 128, 0, st>>>(X, d, perm, off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
     else
-        seg_sum<8><<<maxseg, 128, 0, st>>>(X, d, perm, w.off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
+        seg_sum<8><<<maxseg, 128, 0, st>>>(X, d, perm, off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
     note_launch();
     seg_fold<<<K, 128, 0, st>>>(w.P, w.msegoff, w.nseg, d, S);
     note_launch();

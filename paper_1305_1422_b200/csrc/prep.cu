@@ -119,10 +119,14 @@ __global__ void cb_rowstats(const float *__restrict__ W, int K, int d, const flo
     int lane = threadIdx.x & 31;
     if (j >= K) return;
     const float *w = W + (int64_t)j * d;
+    const float *w0 = W;
     double n2 = 0.0, cm = 0.0, sq = 0.0;
     float amax = 0.0f;
+    bool same0 = j > 0;
     for (int k = lane; k < d; k += 32) {
-        double wv = (double)w[k];
+        float wf = w[k];
+        same0 &= __float_as_uint(wf) == __float_as_uint(w0[k]);
+        double wv = (double)wf;
         double dl = wv - (double)mu[k];
         n2 += dl * dl;
         cm += mu_nu[k] * dl;
@@ -133,8 +137,14 @@ __global__ void cb_rowstats(const float *__restrict__ W, int K, int d, const flo
     cm = warp_sum(cm);
     sq = warp_sum(sq);
     amax = warp_max(amax);
+    // A node bit-identical to node 0 ties it exactly in every distance, and
+    // ties resolve to the lowest index (kernels.py:27-28): mask it out of the
+    // screen (c = +inf).  Covers the collapsed maps of SURVEY.md A.8.
+    same0 = __all_sync(0xffffffffu, same0);
     if (lane == 0) {
-        c[j] = (float)(n2 + 2.0 * cm);
+        float cj = (float)(n2 + 2.0 * cm);
+        c[j] = same0 ? INFINITY : cj;
+        atomic_max_nonneg(&stats[2], fabsf(cj));
         w2[j] = sq;
         float nr = (float)sqrt(n2);
         nrm_out[j] = nr;
@@ -159,9 +169,11 @@ __global__ void cb_pack(const float *__restrict__ W, int K, int d, const float *
     int lane = threadIdx.x & 31;
     if (j >= kp) return;
     int sexp = pick_exp(stats[1]);
-    __half *o = Wh + (int64_t)j * dp;
+    __half *o = Wh ? Wh + (int64_t)j * dp : nullptr;
     __half *ol = Wl ? Wl + (int64_t)j * dp : nullptr;
-    if (j < K) {
+    if (o == nullptr) {
+        if (j >= K && lane == 0) c[j] = INFINITY;
+    } else if (j < K) {
         const float *w = W + (int64_t)j * d;
         double sc = ldexp(1.0, sexp);
         for (int k = lane; k < dp; k += 32) {
@@ -183,6 +195,7 @@ __global__ void cb_pack(const float *__restrict__ W, int K, int d, const float *
         scal[1] = stats[0];     // max_j |delta_j|
         scal[2] = (float)sexp;
         scal[3] = stats[1];
+        scal[4] = stats[2];     // max_j |c_j| (fp32 rounding slack of the sparse window)
     }
 }
 
@@ -246,6 +259,7 @@ extern "C" int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const
     cb_rowstats<<<(K + 7) / 8, 256, 0, st>>>(W, K, d, mu, mu_nu, c, w2, nrm, stats);
     note_launch();
     cb_pack<<<(kp + 7) / 8, 256, 0, st>>>(W, K, d, mu, xexp, (__half *)Wh, (__half *)Wl, dp, kp, c, stats, scal);
+    // (Wh may be NULL: the sparse path screens against a transposed fp32 copy)
     note_launch();
     SOMB_LAUNCH_CHECK("somb_codebook_prepare");
     return SOMB_OK;

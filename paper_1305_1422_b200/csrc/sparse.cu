@@ -1,0 +1,237 @@
+// Sparse (CSR) BMU search and node sums (kernels.py:208-222, 229-242, 315-321).
+//
+// Screen: dots_ij = sum_{k in nz(i)} v_k delta_j[k] against the centred
+// codebook stored TRANSPOSED (dT[k][j] = w_jk - mu_k, fp32, pitch kp), so each
+// nonzero gathers one contiguous node slice; r_ij = c_j - 2 dots_ij with
+// c_j = |delta_j|^2 + 2 mu.delta_j (prep with nu = 0).  One warp per row, 8
+// nodes per lane per 256-node step, fp32 FMA.  The window is rigorous for
+// this arithmetic: |r~ - r| <= 2 (nnz + 2) 2^-24 sum|x||delta| + rounding of
+// c, bounded through Cauchy-Schwarz by coef * |x_i| * max_j |delta_j|.
+// Candidates are collected warp-cooperatively in ascending node order with
+// the same window/cap semantics as the dense screen (cand.cuh), then the exact
+// fp64 re-rank evaluates the reference's sparse formula (x2 - 2 dots) + w2.
+#include "cand.cuh"
+
+namespace somb {
+
+constexpr int SP_WARPS = 8;
+constexpr int SP_NNZ_BUF = 256;      // staged (col, val) pairs per warp
+
+// dT[k][j] = fp32(w_jk - mu_k) for j < K, 0 for padding (prepare-time transpose)
+__global__ void sp_transpose(const float *__restrict__ W, const float *__restrict__ mu, int K, int d, int kp,
+                             float *__restrict__ dT) {
+    __shared__ float tile[32][33];
+    const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+    for (int r = ty; r < 32; r += 8) {
+        int j = j0 + r, k = k0 + tx;
+        tile[r][tx] = (j < K && k < d) ? (float)((double)W[(int64_t)j * d + k] - (double)mu[k]) : 0.0f;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        int k = k0 + r, j = j0 + tx;
+        if (k < d && j < kp) dT[(int64_t)k * kp + j] = tile[tx][r];
+    }
+}
+
+__global__ void sp_row_norms(const int64_t *__restrict__ rowptr, const float *__restrict__ val, int64_t n,
+                             double *__restrict__ x2, float *__restrict__ xnorm, int *__restrict__ nnz_max) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {   // np.add.at order (kernels.py:315-321)
+        double v = (double)val[e];
+        s += v * v;
+    }
+    x2[i] = s;
+    xnorm[i] = (float)sqrt(s);
+    atomicMax(nnz_max, (int)(rowptr[i + 1] - rowptr[i]));
+}
+
+__global__ void __launch_bounds__(32 * SP_WARPS)
+sp_screen_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col, const float *__restrict__ val,
+                 int64_t n, const float *__restrict__ dT, int kp, const float *__restrict__ c,
+                 const float *__restrict__ xnorm, const float *__restrict__ scal, float wcoef,
+                 int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags) {
+    __shared__ int s_col[SP_WARPS][SP_NNZ_BUF];
+    __shared__ float s_val[SP_WARPS][SP_NNZ_BUF];
+    __shared__ float s_bv[SP_WARPS][SOMB_CAND_CAP];
+    __shared__ int s_bi[SP_WARPS][SOMB_CAND_CAP];
+    const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * SP_WARPS + w;
+    if (row >= n) return;
+    const int64_t e0 = rowptr[row], e1 = rowptr[row + 1];
+    const int nnz = (int)(e1 - e0);
+    const float nmax = scal[1];
+    CandRow<SOMB_CAND_CAP> st;   // meaningful in lane 0 only
+    cand_init(st, wcoef * (float)(nnz + 2) * xnorm[row] * nmax + ldexpf(scal[4], -21));
+    const CandBuf cb{smem_addr(&s_bv[w][0]), smem_addr(&s_bi[w][0]), 4u};
+    float thr = st.thr;
+    for (int j0 = 0; j0 < kp; j0 += 256) {
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+        const int jl = j0 + lane * 8;
+        for (int b0 = 0; b0 < nnz; b0 += SP_NNZ_BUF) {
+            const int m = min(SP_NNZ_BUF, nnz - b0);
+            __syncwarp();
+            for (int t = lane; t < m; t += 32) {
+                s_col[w][t] = col[e0 + b0 + t];
+                s_val[w][t] = val[e0 + b0 + t];
+            }
+            __syncwarp();
+            for (int t = 0; t < m; ++t) {
+                const float v = s_val[w][t];
+                const float4 *p = reinterpret_cast<const float4 *>(dT + (int64_t)s_col[w][t] * kp + jl);
+                float4 a = __ldg(p), b = __ldg(p + 1);
+                acc[0] = fmaf(v, a.x, acc[0]); acc[1] = fmaf(v, a.y, acc[1]);
+                acc[2] = fmaf(v, a.z, acc[2]); acc[3] = fmaf(v, a.w, acc[3]);
+                acc[4] = fmaf(v, b.x, acc[4]); acc[5] = fmaf(v, b.y, acc[5]);
+                acc[6] = fmaf(v, b.z, acc[6]); acc[7] = fmaf(v, b.w, acc[7]);
+            }
+        }
+        const float4 *cp = reinterpret_cast<const float4 *>(c + jl);
+        float4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
+        float r[8] = {fmaf(-2.0f, acc[0], c0.x), fmaf(-2.0f, acc[1], c0.y), fmaf(-2.0f, acc[2], c0.z),
+                      fmaf(-2.0f, acc[3], c0.w), fmaf(-2.0f, acc[4], c1.x), fmaf(-2.0f, acc[5], c1.y),
+                      fmaf(-2.0f, acc[6], c1.z), fmaf(-2.0f, acc[7], c1.w)};
+        float lo = fminf(fminf(fminf(r[0], r[1]), fminf(r[2], r[3])), fminf(fminf(r[4], r[5]), fminf(r[6], r[7])));
+        unsigned hit = __ballot_sync(0xffffffffu, lo <= thr);
+        if (hit) {
+            // visit the hit lanes in ascending node order; lane 0 owns the row state
+            while (hit) {
+                const int src = __ffs(hit) - 1;
+                hit &= hit - 1;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float vq = __shfl_sync(0xffffffffu, r[q], src);
+                    if (lane == 0 && vq <= st.thr) cand_push<SOMB_CAND_CAP>(st, vq, j0 + src * 8 + q, cb);
+                }
+            }
+            thr = __shfl_sync(0xffffffffu, st.thr, 0);
+        }
+    }
+    if (lane == 0) {
+        ccount[row] = cand_emit<SOMB_CAND_CAP>(st, cb, cand + row * SOMB_CAND_CAP);
+        flags[row] = st.trunc;
+    }
+}
+
+// Exact fp64 re-rank with the reference's sparse formula:
+// d2 = (x2 - 2 sum_t v_t w_j[col_t]) + w2_j, clamp >= 0 (kernels.py:216-219).
+__global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col,
+                                 const float *__restrict__ val, int64_t n, int d, const float *__restrict__ W,
+                                 const double *__restrict__ w2, int K, const double *__restrict__ x2,
+                                 const int *__restrict__ cand, const int *__restrict__ ccount, int all,
+                                 int *__restrict__ bmu, double *__restrict__ d2min) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const int64_t e0 = rowptr[row], e1 = rowptr[row + 1];
+    int cnt = all ? 0 : ccount[row];
+    const bool scan = all || cnt <= 0;
+    if (scan) cnt = K;
+    double best = INFINITY;
+    int bestj = 0x7fffffff;
+    const double xx = x2[row];
+    for (int q = 0; q < cnt; ++q) {
+        const int j = scan ? q : cand[row * SOMB_CAND_CAP + q];
+        if ((unsigned)j >= (unsigned)K) continue;
+        const float *wr = W + (int64_t)j * d;
+        double s = 0.0;
+        for (int64_t e = e0 + lane; e < e1; e += 32) s = __fma_rn((double)val[e], (double)wr[col[e]], s);
+        s = warp_sum(s);
+        double v = fmax(__dadd_rn(__dsub_rn(xx, __dmul_rn(2.0, s)), w2[j]), 0.0);
+        if (v < best || (v == best && j < bestj)) {
+            best = v;
+            bestj = j;
+        }
+    }
+    if (lane == 0) {
+        bmu[row] = bestj;
+        d2min[row] = best;
+    }
+}
+
+// S_b = sum of the rows of node b in ascending row order (sparse scatter into
+// the dense fp64 K x d accumulator; a row's columns are unique, so the threads
+// of a block never collide); kernels.py:229-242 regrouped by BMU.
+__global__ void sp_node_sums_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col,
+                                    const float *__restrict__ val, int d, const int *__restrict__ perm,
+                                    const int *__restrict__ off, int K, double *__restrict__ S) {
+    const int b = blockIdx.x;
+    if (b >= K) return;
+    double *sb = S + (int64_t)b * d;
+    for (int t = off[b]; t < off[b + 1]; ++t) {
+        const int i = perm[t];
+        for (int64_t e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x) sb[col[e]] += (double)val[e];
+        __syncthreads();
+    }
+}
+
+int node_bucket_sort(const int *bmu, int64_t n, int K, void *ws, const int **perm, const int **off, double *cnt,
+                     cudaStream_t st);
+
+}  // namespace somb
+
+using namespace somb;
+
+extern "C" int somb_sparse_row_stats(const int64_t *rowptr, const float *val, int64_t n, double *x2, float *xnorm,
+                                     int32_t *nnz_max, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    cudaMemsetAsync(nnz_max, 0, sizeof(int), st);
+    if (n == 0) return SOMB_OK;
+    sp_row_norms<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rowptr, val, n, x2, xnorm, nnz_max);
+    note_launch();
+    SOMB_LAUNCH_CHECK("sparse_row_stats");
+    return SOMB_OK;
+}
+
+extern "C" int somb_sparse_codebook_T(const float *W, const float *mu, int32_t K, int32_t d, int32_t kp, float *dT,
+                                      void *stream) {
+    SOMB_REQUIRE(kp % 256 == 0 && kp >= K, SOMB_E_INPUT, "sparse_codebook_T: kp must be a multiple of 256");
+    dim3 g((kp + 31) / 32, (d + 31) / 32);
+    sp_transpose<<<g, dim3(32, 8), 0, as_stream(stream)>>>(W, mu, K, d, kp, dT);
+    note_launch();
+    SOMB_LAUNCH_CHECK("sparse_codebook_T");
+    return SOMB_OK;
+}
+
+extern "C" int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const float *val, int64_t n, int32_t d,
+                               const float *dT, const float *W, const float *c, const double *w2, int32_t K,
+                               int32_t kp, const float *scal, const double *x2, const float *xnorm, float window_coef,
+                               int32_t exact, int32_t *bmu, double *d2min, int32_t *flags, void *ws, void *stream) {
+    SOMB_REQUIRE(K > 0 && d > 0 && kp % 256 == 0, SOMB_E_INPUT, "bmu_sparse: bad shape");
+    if (n == 0) return SOMB_OK;
+    cudaStream_t st = as_stream(stream);
+    int *cand = (int *)ws;
+    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
+    if (!exact) {
+        sp_screen_kernel<<<(unsigned)((n + SP_WARPS - 1) / SP_WARPS), 32 * SP_WARPS, 0, st>>>(
+            rowptr, col, val, n, dT, kp, c, xnorm, scal, window_coef, cand, ccount, flags);
+        note_launch();
+    } else {
+        cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
+    }
+    sp_rerank_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(rowptr, col, val, n, d, W, w2, K, x2, cand, ccount,
+                                                              exact, bmu, d2min);
+    note_launch();
+    SOMB_LAUNCH_CHECK("bmu_sparse");
+    return SOMB_OK;
+}
+
+extern "C" int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col, const float *val, int64_t n,
+                                     int32_t d, const int32_t *bmu, int32_t K, double *S, double *cnt, void *ws,
+                                     void *stream) {
+    SOMB_REQUIRE(K > 0 && d > 0 && n < (1ll << 31), SOMB_E_INPUT, "node_sums_sparse: bad shape");
+    cudaStream_t st = as_stream(stream);
+    cudaMemsetAsync(S, 0, (size_t)K * d * sizeof(double), st);
+    const int *perm = nullptr, *off = nullptr;
+    int rc = node_bucket_sort(bmu, n, K, ws, &perm, &off, cnt, st);
+    if (rc) return rc;
+    if (n == 0) return SOMB_OK;
+    sp_node_sums_kernel<<<K, 256, 0, st>>>(rowptr, col, val, d, perm, off, K, S);
+    note_launch();
+    SOMB_LAUNCH_CHECK("node_sums_sparse");
+    return SOMB_OK;
+}

@@ -86,20 +86,13 @@ class SomEngine:
         self.opt = options or EngineOptions()
         self.group = group
         self.rank, self.world = dist_info(group)
-        if isinstance(data, SparseDataset):
-            raise errors.KernelDataMismatch("SomEngine(dense): got sparse data")
         self.nx, self.ny = int(n_columns), int(n_rows)
         self.K = self.nx * self.ny
         self.map_type, self.grid = map_type, grid
         self.cmap = _lib.SombMap(self.nx, self.ny,
                                  _lib.GRID_HEX if grid is GridType.HEXAGONAL else _lib.GRID_RECT,
                                  _lib.TOROID if map_type is MapType.TOROID else _lib.PLANAR)
-        x = data.values if isinstance(data, DenseDataset) else data
-        self._upload_dense(x, dry=True)
-        dp0 = _round_up(self.d, 8)
-        p = self.opt.screen_passes
-        self.passes = 3 if (p == 3 or (p == 0 and dp0 <= 256)) and self.opt.screen == "tensor" else 1
-        self.pack_dataset()
+        self._init_data(data)
         d = self.d
         self.dp = _round_up(d, 8)
         self.kp = _round_up(self.K, 256)
@@ -111,12 +104,10 @@ class SomEngine:
         f32, f64, dev = torch.float32, torch.float64, self.dev
         self.W = torch.zeros((self.kpad, d), dtype=f32, device=dev)
         self.W2 = torch.zeros((self.kpad, d), dtype=f32, device=dev)
-        self.Wh = torch.empty((self.kp, self.dp), dtype=torch.float16, device=dev)
-        self.Wl = (torch.empty((self.kp, self.dp), dtype=torch.float16, device=dev)
-                   if self.passes == 3 else None)
+        self._init_codebook_buffers()
         self.c = torch.empty(self.kp, dtype=f32, device=dev)
         self.w2 = torch.empty(self.K, dtype=f64, device=dev)
-        self.scal = torch.empty(4, dtype=f32, device=dev)
+        self.scal = torch.zeros(8, dtype=f32, device=dev)
         n = self.n
         self.bmu = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         self.d2min = torch.empty(max(n, 1), dtype=f64, device=dev)
@@ -134,13 +125,32 @@ class SomEngine:
                  lib.somb_node_sums_ws(n, d, self.K),
                  lib.somb_hood_ws(C.byref(self.cmap), self.K, d), 1 << 16)
         self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)
-        if self.passes == 3:
-            kappa = self.opt.window_kappa3 if self.opt.window_kappa3 is not None else _kappa3(d)
-        else:
-            kappa = self.opt.window_kappa
-        self.window_coef = float(kappa * _U16 / math.sqrt(d))
+        self.window_coef = self._window_coef()
         self.screen_impl = {"tensor": 0, "simt": 1, "exact": 2}[self.opt.screen]
         self.has_prev = False
+
+    # ------------------------------------------------------- subclass hooks
+    def _init_data(self, data):
+        if isinstance(data, SparseDataset):
+            raise errors.KernelDataMismatch("SomEngine(dense): got sparse data")
+        x = data.values if isinstance(data, DenseDataset) else data
+        self._upload_dense(x, dry=True)
+        dp0 = _round_up(self.d, 8)
+        p = self.opt.screen_passes
+        self.passes = 3 if (p == 3 or (p == 0 and dp0 <= 256)) and self.opt.screen == "tensor" else 1
+        self.pack_dataset()
+
+    def _init_codebook_buffers(self):
+        self.Wh = torch.empty((self.kp, self.dp), dtype=torch.float16, device=self.dev)
+        self.Wl = (torch.empty((self.kp, self.dp), dtype=torch.float16, device=self.dev)
+                   if self.passes == 3 else None)
+
+    def _window_coef(self) -> float:
+        if self.passes == 3:
+            kappa = self.opt.window_kappa3 if self.opt.window_kappa3 is not None else _kappa3(self.d)
+        else:
+            kappa = self.opt.window_kappa
+        return float(kappa * _U16 / math.sqrt(self.d))
 
     # ------------------------------------------------------------ dataset
     def _upload_dense(self, x, dry=False):

@@ -64,12 +64,16 @@ def test_search_accumulate_golden(screen):
     for ci in range(int(g["ncases"])):
         n, d, nx, ny, tor, radius, cutoff, kern, scale = g[f"c{ci}_params"]
         n, d, nx, ny, kern = int(n), int(d), int(nx), int(ny), int(kern)
+        w = g[f"c{ci}_w"]
         if kern == 2:
-            continue
-        x, w = g[f"c{ci}_x"], g[f"c{ci}_w"]
+            if screen == "simt":
+                continue        # the sparse path has its own gather screen
+            data = S.SparseDataset(d, g[f"c{ci}_offsets"], g[f"c{ci}_cols"], g[f"c{ci}_vals"])
+        else:
+            data = S.DenseDataset(g[f"c{ci}_x"])
         cb = S.CodeBook(nx, ny, d, w)
         mt = S.MapType.TOROID if tor else S.MapType.PLANAR
-        bmu, qe, acc = S.search_accumulate(S.DenseDataset(x), cb, radius, cutoff, mt,
+        bmu, qe, acc = S.search_accumulate(data, cb, radius, cutoff, mt,
                                            S.Kernel(kern), options=_opts(screen))
         assert np.array_equal(bmu, g[f"c{ci}_bmu"]), (ci, np.sum(bmu != g[f"c{ci}_bmu"]))
         assert qe == pytest.approx(float(g[f"c{ci}_qe"]), rel=1e-12)
@@ -297,3 +301,54 @@ def test_cfg2_shape_teacher_forced_epochs():
         assert_bmus_tie_aware(bmu_g, ob, x, w)
         assert rel_err(got, want) <= 1e-6, e
         w = want
+
+
+def _csr(x, keep):
+    """CSR of x with entries where keep is False dropped (sorted unique cols)."""
+    rows, cols = np.nonzero(keep)
+    offs = np.zeros(x.shape[0] + 1, np.int64)
+    np.add.at(offs, rows + 1, 1)
+    offs = np.cumsum(offs)
+    return S.SparseDataset(x.shape[1], offs, cols.astype(np.int32), x[rows, cols].astype(np.float32))
+
+
+@pytest.mark.parametrize("screen", ["tensor", "exact"])
+def test_sparse_hand_cases(screen):
+    # reference tests/test_kernels.py:41-62 with the sparse kernel
+    cb = S.CodeBook(2, 1, 2, np.array([[0, 0], [1, 1]], np.float32))
+    x = np.array([[0.4, 0.4], [0.6, 0.6], [0.1, 0.0]], np.float32)
+    assert S.bmu_search_sparse(_csr(x, x != 0), cb, options=_opts(screen)).tolist() == [[0, 0], [0, 1], [0, 0]]
+    w = np.array([[9, 9], [0.5, 0.5], [8, 8], [0.5, 0.5]], np.float32)
+    x = np.array([[0.5, 0.5]], np.float32)
+    assert S.bmu_search_sparse(_csr(x, x != 0), S.CodeBook(2, 2, 2, w), options=_opts(screen)).tolist() == [[0, 1]]
+
+
+@pytest.mark.parametrize("screen", ["tensor", "exact"])
+def test_sparse_train_golden(screen):
+    g = golden("sparse_train.npz")
+    for s_ in ("s0", "s1"):
+        e, nx, ny, tor = (int(v) for v in g[f"{s_}_cfg"])
+        d = 40 if s_ == "s0" else 500
+        data = S.SparseDataset(d, g[f"{s_}_offsets"], g[f"{s_}_cols"], g[f"{s_}_vals"])
+        cfg = S.TrainConfig(n_epochs=e, n_columns=nx, n_rows=ny, kernel=S.Kernel.SPARSE,
+                            map_type=S.MapType.TOROID if tor else S.MapType.PLANAR)
+        init = S.CodeBook(nx, ny, d, g["s0_w0"]) if s_ == "s0" else None
+        cb, bmus, u = S.train(data, cfg, initial_codebook=init, options=_opts(screen))
+        assert np.array_equal(bmus, g[f"{s_}_bmus"]), s_
+        assert rel_err(cb.weights, g[f"{s_}_w"]) <= 1e-6, s_
+        np.testing.assert_allclose(u.heights, g[f"{s_}_u"], rtol=1e-5, atol=1e-9)
+
+
+def test_sparse_random_vs_oracle():
+    rng = np.random.default_rng(21)
+    sp = O.gen_random_sparse(3000, 4000, 0.01, 5)
+    data = S.SparseDataset(sp.n_dimensions, sp.row_offsets, sp.col_indices, sp.values)
+    dense = sp.densify()
+    w = dense[rng.choice(3000, 300, replace=False)].copy()      # data-sampled, non-degenerate
+    cb = S.CodeBook(20, 15, 4000, w)
+    bmu, qe, acc = S.search_accumulate(data, cb, 3.0, 1e-3, S.MapType.PLANAR, S.Kernel.SPARSE)
+    ob, oqe, num, den = O.search_accumulate(sp, w, 20, 15, 3.0, 1e-3, O.PLANAR, O.SPARSE)
+    assert_bmus_tie_aware(bmu, ob, dense, w)
+    assert qe == pytest.approx(oqe, rel=1e-12)
+    np.testing.assert_allclose(acc.numerators, num, rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(acc.denominators, den, rtol=1e-11, atol=1e-12)
