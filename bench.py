@@ -35,6 +35,8 @@ CONFIGS = {
              "cfg1: dense 50x40 planar rect map, 10k x 100 fp32 uniform, gaussian"),
     "cfg2": (1_000_000, 1000, 200, 200, "toroid", "rectangular", "gaussian", False,
              "cfg2: emergent 200x200 toroid, 1M x 1000 fp32 uniform, gaussian"),
+    "cfg3": (500_000, 50_000, 100, 100, "planar", "rectangular", "gaussian", False,
+             "cfg3: sparse 100x100 planar, 500k x 50k CSR, 250 nnz/row (0.5%), gaussian"),
     "cfg4": (2_000_000, 256, 300, 300, "toroid", "hexagonal", "bubble", True,
              "cfg4: hexagonal toroid 300x300, 2M x 256 fp32 uniform, bubble, compact support"),
     "cfg5": (4_000_000, 128, 500, 500, "planar", "rectangular", "gaussian", False,
@@ -118,6 +120,23 @@ def init_dist(args):
     return rank, world, local
 
 
+SPARSE_NNZ = 250
+
+
+def sparse_rows_device(n, d, nnz, seed, dev):
+    """Synthetic text-like CSR rows on the device: nnz distinct sorted columns
+    per row (one uniform pick in each of nnz equal column bins), values U[0,1)."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    width = d // nnz
+    base = torch.arange(nnz, device=dev, dtype=torch.int64) * width
+    cols = (base[None, :] + torch.randint(0, width, (n, nnz), generator=g, device=dev)).to(torch.int32)
+    vals = torch.rand((n, nnz), generator=g, device=dev)
+    rowptr = torch.arange(n + 1, device=dev, dtype=torch.int64) * nnz
+    return rowptr, cols.reshape(-1), vals.reshape(-1)
+
+
 def cpu_reference_rate(cfg_name, n_sub, steps, warmup, seed=1001):
     """Oracle port (numpy restatement of the reference path, kernels.py:365-450)
     on all host cores: search_accumulate(DENSE_BLOCKED) over an n_sub-row
@@ -128,7 +147,12 @@ def cpu_reference_rate(cfg_name, n_sub, steps, warmup, seed=1001):
     import oracle as O
     n, d, nx, ny, mt, grid, nbh, compact, _ = CONFIGS[cfg_name]
     rng = np.random.default_rng(seed)
-    x = rng.random((n_sub, d), dtype=np.float32)
+    if cfg_name == "cfg3":
+        x = O.gen_random_sparse(n_sub, d, SPARSE_NNZ / d, seed)
+        kern = O.SPARSE
+    else:
+        x = rng.random((n_sub, d), dtype=np.float32)
+        kern = O.DENSE_BLOCKED
     w = O.init_codebook(nx, ny, d, 1)
     og = O.HEX if grid == "hexagonal" else O.RECT
     workers = os.cpu_count() or 1
@@ -136,7 +160,7 @@ def cpu_reference_rate(cfg_name, n_sub, steps, warmup, seed=1001):
     for s in range(warmup + steps):
         radius, scale = schedule_for(cfg_name, s)
         t0 = time.perf_counter()
-        _, _, num, den = O.search_accumulate(x, w, nx, ny, radius, 1e-3, mt, O.DENSE_BLOCKED, workers,
+        _, _, num, den = O.search_accumulate(x, w, nx, ny, radius, 1e-3, mt, kern, workers,
                                              True, og, nbh, compact)
         t1 = time.perf_counter()
         w = O.blend(w, num, den, scale)
@@ -148,7 +172,7 @@ def cpu_reference_rate(cfg_name, n_sub, steps, warmup, seed=1001):
     t_epoch = (n / n_sub) * sa + bl
     return {"value": n * nx * ny / t_epoch, "unit": UNIT, "cores": workers, "kind": "port",
             "sample": f"{n_sub} of {n} rows x {nx * ny} nodes x {d} dims: search_accumulate "
-                      f"(DENSE_BLOCKED, {workers} workers) {sa:.2f} s + blend {bl:.2f} s per step, "
+                      f"({'SPARSE' if kern == O.SPARSE else 'DENSE_BLOCKED'}, {workers} workers) {sa:.2f} s + blend {bl:.2f} s per step, "
                       f"median of {len(t_sa[k])}; epoch = N/n_sub * search + blend",
             "seconds_per_step": t_epoch}
 
@@ -183,12 +207,20 @@ def run_ours(args):
     K = nx * ny
     dev = torch.device("cuda", torch.cuda.current_device())
     first, count = S.partition(n, world)[rank]
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1001 + rank)
-    X = torch.rand((count, d), generator=gen, device=dev, dtype=torch.float32)
     opts = EngineOptions(screen=args.screen)
     mtype, gtype, nb = S.MapType(mt), S.GridType(grid), S.Neighborhood(nbh)
-    eng = SomEngine(X, nx, ny, mtype, gtype, device=dev, options=opts)
+    sparse = args.config == "cfg3"
+    if sparse:
+        from paper_1305_1422_b200.sparse import SparseEngine
+        rp, cl, vl = sparse_rows_device(count, d, SPARSE_NNZ, 1001 + rank, dev)
+        sdata = S.SparseDataset(d, rp.cpu().numpy(), cl.cpu().numpy(), vl.cpu().numpy())
+        eng = SparseEngine(sdata, nx, ny, mtype, gtype, device=dev, options=opts)
+        X = None
+    else:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(1001 + rank)
+        X = torch.rand((count, d), generator=gen, device=dev, dtype=torch.float32)
+        eng = SomEngine(X, nx, ny, mtype, gtype, device=dev, options=opts)
     w0 = S.init_codebook(S.TrainConfig(n_columns=nx, n_rows=ny, seed=1), d).weights
     eng.set_codebook(w0)
     lib = _lib.load()
@@ -238,6 +270,9 @@ def run_ours(args):
     flops = 2.0 * count * K * d
     achieved = flops / (scr_ms / 1e3) / 1e12
     peak_sus = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    if sparse:   # gather-bound: report the gathered codebook bytes against HBM
+        gathered = float(count) * SPARSE_NNZ * eng.kp * 4
+        achieved_gbs = gathered / (scr_ms / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_screen_{args.config}.json")
     if os.path.exists(tpath):
@@ -245,11 +280,18 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": "screen_tc_kernel (tcgen05 kind::f16)",
+    roofline = {"bound": "tensor", "kernel": "screen_tc2_kernel (tcgen05 cta_group::2 kind::f16)",
                 "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
                 "peak_kind": f"{pk_kind} bf16 dense sustained (fp16 kind::f16 runs at the bf16 rate)",
                 "frac_of_burst": achieved / pk.get("bf16_tflops", peak_sus),
-                "traffic": traffic, "flops_per_launch": flops, "avg_launch_ms": scr_ms}
+                "traffic": traffic, "flops_per_launch": flops, "avg_launch_ms": scr_ms,
+                "screen_passes": getattr(eng, "passes", 1)}
+    if sparse:
+        roofline = {"bound": "hbm", "kernel": "sp_screen_kernel (fp32 gather over the transposed codebook)",
+                    "achieved": achieved_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved_gbs / pk["hbm_gbs"], "traffic": traffic,
+                    "bytes_per_launch": gathered, "avg_launch_ms": scr_ms,
+                    "note": "algorithmic bytes = nnz x kp x 4 gathered codebook values"}
 
     # per-phase breakdown (rank-local averages)
     phases = {k: statistics.mean(v) for k, v in phase_ms.items() if v}
@@ -259,17 +301,21 @@ def run_ours(args):
     # end to end through the public API: host (pinned) data -> train() -> host results
     e2e = None
     if not args.no_e2e:
-        Xh = torch.empty((count, d), dtype=torch.float32, pin_memory=True)
-        Xh.copy_(X)
+        if sparse:
+            data = sdata
+        else:
+            Xh = torch.empty((count, d), dtype=torch.float32, pin_memory=True)
+            Xh.copy_(X)
+            data = S.DenseDataset(Xh)
         del eng
+        X = None
         torch.cuda.empty_cache()
+        kern = S.Kernel.SPARSE if sparse else S.Kernel.DENSE_BLOCKED
         cfg = S.TrainConfig(n_epochs=args.e2e_epochs, n_columns=nx, n_rows=ny, map_type=mtype,
-                            kernel=S.Kernel.DENSE_BLOCKED, grid=gtype, neighborhood=nb,
-                            compact_support=compact, seed=1)
-        data = S.DenseDataset(Xh)
-        S.train(data, S.TrainConfig(n_epochs=1, n_columns=nx, n_rows=ny, map_type=mtype,
-                                    kernel=S.Kernel.DENSE_BLOCKED, grid=gtype, neighborhood=nb,
-                                    compact_support=compact), options=opts, local_rows=True)
+                            kernel=kern, grid=gtype, neighborhood=nb, compact_support=compact, seed=1)
+        S.train(data, S.TrainConfig(n_epochs=1, n_columns=nx, n_rows=ny, map_type=mtype, kernel=kern,
+                                    grid=gtype, neighborhood=nb, compact_support=compact),
+                options=opts, local_rows=True)
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
@@ -282,7 +328,8 @@ def run_ours(args):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         te = float(te.item())
         e2e = {"value": n * K * args.e2e_epochs / te, "unit": UNIT,
-               "h2d_bytes_per_step": int(count * d * 4 + K * d * 4),
+               "h2d_bytes_per_step": int((count * SPARSE_NNZ * 8 + (count + 1) * 8 if sparse else count * d * 4)
+                                         + K * d * 4),
                "d2h_bytes_per_step": int(K * d * 4 + n * 2 * 4 + K * 4),
                "step": f"one public train() call: H2D of the rank's rows from pinned memory, "
                        f"{args.e2e_epochs} epochs, final naive BMU pass, U-matrix, D2H of "
@@ -329,10 +376,12 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--screen", default="tensor", choices=["tensor", "simt", "exact"])
     ap.add_argument("--e2e-epochs", type=int, default=10)
-    ap.add_argument("--ref-rows", type=int, default=4096)
+    ap.add_argument("--ref-rows", type=int, default=0, help="CPU sample rows (0: per-config default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.ref_rows == 0:
+        args.ref_rows = {"cfg3": 256, "cfg5": 512, "cfg4": 1024, "cfg1": 10000}.get(args.config, 4096)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
