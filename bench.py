@@ -295,6 +295,9 @@ def run_ours(args):
 
     # per-phase breakdown (rank-local averages)
     phases = {k: statistics.mean(v) for k, v in phase_ms.items() if v}
+    cc = eng.candidate_counts()[: eng.n].float().cpu().numpy() if eng.n else np.zeros(1)
+    cand_stats = {"mean": float(cc.mean()), "p50": float(np.median(cc)), "p99": float(np.percentile(cc, 99)),
+                  "max": float(cc.max())}
     flags = eng.flags[: eng.n].cpu().numpy()
     trunc = float(((flags & 0xFF) | ((flags >> 8) & 0xFF)).astype(bool).mean()) if eng.n else 0.0
 
@@ -358,7 +361,8 @@ def run_ours(args):
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
                 "gpu_launches": int(launches),
                 "phase_ms": phases, "epoch_ms": ms_step,
-                "nkd_per_s": value * d, "window_truncated_rows": trunc}
+                "nkd_per_s": value * d, "window_truncated_rows": trunc,
+                "candidates_per_row": cand_stats}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

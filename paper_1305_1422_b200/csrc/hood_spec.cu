@@ -83,10 +83,98 @@ __global__ void __launch_bounds__(256) dgemm_fn(int M, int N, int Kd, AL al, BL 
     }
 }
 
+// FP64 tensor-core variant: mma.sync.m8n8k4.f64 (DMMA).  Block tile 64 x 64
+// x 16, four warps of 32 x 32 (4 x 4 m8n8 fragments); next k-tile prefetched
+// into registers while the current one is multiplied.  Same loader /
+// epilogue interface as dgemm_fn.
+constexpr int TM = 64, TN = 64, TK = 16, TPAD = 8;
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+template <class AL, class BL, class EP>
+__global__ void __launch_bounds__(128) dgemm_mma_fn(int M, int N, int Kd, AL al, BL bl, EP ep) {
+    __shared__ double sa[TK][TM + TPAD];   // A tile stored k-major: sa[k][m]
+    __shared__ double sb[TK][TN + TPAD];   // B tile: sb[k][n]
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int b = blockIdx.z;
+    const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double ra[8], rb[8];   // 1024 A + 1024 B elements per tile / 128 threads
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            int e = t + 128 * q;            // 0..1023
+            int kk = e / TM, mm = e % TM;
+            int m = m0 + mm, k = k0 + kk;
+            ra[q] = (m < M && k < Kd) ? al(b, m, k) : 0.0;
+            int kb = e / TN, nn = e % TN;
+            int n = n0 + nn, k2 = k0 + kb;
+            rb[q] = (n < N && k2 < Kd) ? bl(b, k2, n) : 0.0;
+        }
+    };
+    fetch(0);
+    for (int k0 = 0; k0 < Kd; k0 += TK) {
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            int e = t + 128 * q;
+            sa[e / TM][e % TM] = ra[q];
+            sb[e / TN][e % TN] = rb[q];
+        }
+        __syncthreads();
+        if (k0 + TK < Kd) fetch(k0 + TK);
+#pragma unroll
+        for (int ks = 0; ks < TK; ks += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = sa[ks + (lane & 3)][wm + 8 * i + (lane >> 2)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = sb[ks + (lane & 3)][wn + 8 * j + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma884(acc[i][j], af[i], bf[j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int m = m0 + wm + 8 * i + (lane >> 2);
+        if (m >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                int n = n0 + wn + 8 * j + 2 * (lane & 3) + h;
+                if (n < N) ep(b, m, n, acc[i][j][h]);
+            }
+        }
+    }
+}
+
+static int g_dgemm_impl = -1;   // SOMB_DGEMM=dfma selects the DFMA tiles (A/B testing)
+
 template <class AL, class BL, class EP>
 static void dgemm_launch(int batch, int M, int N, int Kd, AL al, BL bl, EP ep, cudaStream_t st) {
-    dim3 g((N + GN - 1) / GN, (M + GM - 1) / GM, batch);
-    dgemm_fn<<<g, 256, 0, st>>>(M, N, Kd, al, bl, ep);
+    if (g_dgemm_impl < 0) {
+        const char *e = getenv("SOMB_DGEMM");
+        g_dgemm_impl = (e && strcmp(e, "dfma") == 0) ? 0 : 1;
+    }
+    if (g_dgemm_impl == 1) {
+        dim3 g((N + TN - 1) / TN, (M + TM - 1) / TM, batch);
+        dgemm_mma_fn<<<g, 128, 0, st>>>(M, N, Kd, al, bl, ep);
+    } else {
+        dim3 g((N + GN - 1) / GN, (M + GM - 1) / GM, batch);
+        dgemm_fn<<<g, 256, 0, st>>>(M, N, Kd, al, bl, ep);
+    }
     note_launch();
 }
 
