@@ -69,7 +69,7 @@ typedef struct somb_hood {
 #define SOMB_CONV_SPECTRAL 2    /* fp64 DFT along x + per-frequency GEMM    */
 
 /* Screening parameters of the tensor-core BMU search. */
-#define SOMB_CAND_CAP 32        /* candidates kept per row               */
+#define SOMB_CAND_CAP 64        /* candidates kept per row (2 x 32 column groups) */
 
 SOMB_API const char *somb_version(void);
 SOMB_API const char *somb_last_error(void);

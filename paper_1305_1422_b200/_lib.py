@@ -20,7 +20,7 @@ GRID_RECT, GRID_HEX = 0, 1
 PLANAR, TOROID = 0, 1
 NBH_GAUSSIAN, NBH_BUBBLE = 0, 1
 DIST_NAIVE, DIST_BLOCKED = 0, 1
-CAND_CAP = 32
+CAND_CAP = 64
 
 
 class SombMap(C.Structure):

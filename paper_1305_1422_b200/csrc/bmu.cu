@@ -75,6 +75,7 @@ __global__ void screen_seed_kernel(const __half *__restrict__ Xh, const __half *
 constexpr int kSimtRows = 128;
 constexpr int kSimtCols = 32;
 constexpr int kSimtK = 64;
+constexpr int kSimtCap = 32;   // candidates per row of the reference screen (<= SOMB_CAND_CAP)
 
 __global__ void __launch_bounds__(kSimtRows)
 screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __half *__restrict__ Wh,
@@ -82,14 +83,14 @@ screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __hal
                    const float *__restrict__ scal, float wcoef, const float *__restrict__ thr0,
                    int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags) {
     __shared__ float wt[kSimtCols][kSimtK + 1];
-    __shared__ float bv[SOMB_CAND_CAP * kSimtRows];
-    __shared__ int bi[SOMB_CAND_CAP * kSimtRows];
+    __shared__ float bv[kSimtCap * kSimtRows];
+    __shared__ int bi[kSimtCap * kSimtRows];
     const int t = threadIdx.x;
     const int64_t row = (int64_t)blockIdx.x * kSimtRows + t;
     const bool live = row < n;
     const float m = scal[0];
     const float nmax = scal[1];
-    CandRow<SOMB_CAND_CAP> st;
+    CandRow<kSimtCap> st;
     cand_init(st, live ? wcoef * xnorm[row] * nmax : 0.0f);
     if (live && thr0) st.thr = thr0[row];
     const CandBuf cb{smem_addr(bv + t), smem_addr(bi + t), 4u * kSimtRows};
@@ -124,13 +125,13 @@ screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __hal
 #pragma unroll 1
             for (int q = 0; q < kSimtCols; ++q) {
                 float r = fmaf(acc[q], m, c[j0 + q]);
-                cand_push<SOMB_CAND_CAP>(st, r, j0 + q, cb);
+                cand_push<kSimtCap>(st, r, j0 + q, cb);
             }
         }
     }
     if (live) {
         int *out = cand + row * SOMB_CAND_CAP;
-        ccount[row] = cand_emit<SOMB_CAND_CAP>(st, cb, out);
+        ccount[row] = cand_emit<kSimtCap>(st, cb, out);
         flags[row] = st.trunc;
     }
 }
@@ -239,18 +240,24 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
     const int c0 = split ? (cc & 255) : cc;
     const int c1 = split ? ((cc >> 8) & 255) : 0;
     int cnt = c0 + c1;
-    int myj = -1;
-    if (lane < cnt) myj = cand[row * SOMB_CAND_CAP + (lane < c0 ? lane : SOMB_CAND_CAP / 2 + (lane - c0))];
+    // candidate q lives in lane q % 32, register q / 32 (up to 64 per row)
+    auto slot = [&](int q) { return q < c0 ? q : SOMB_CAND_CAP / 2 + (q - c0); };
+    int myj0 = lane < cnt ? cand[row * SOMB_CAND_CAP + slot(lane)] : -1;
+    int myj1 = lane + 32 < cnt ? cand[row * SOMB_CAND_CAP + slot(lane + 32)] : -1;
+    auto cand_at = [&](int q) {
+        int a = __shfl_sync(0xffffffffu, myj0, q & 31), b = __shfl_sync(0xffffffffu, myj1, q & 31);
+        return q < 32 ? a : b;
+    };
     const bool all = cnt <= 0;       // safety net: exact scan of every node
     if (all) cnt = K;
     const double xx = x2[row];
     double best = INFINITY;
     int bestj = 0x7fffffff;
-    int j = all ? 0 : __shfl_sync(0xffffffffu, myj, 0);
+    int j = all ? 0 : cand_at(0);
     float4 wv[Q];
     load_row4<Q>(W, (unsigned)j < (unsigned)K ? j : 0, d4, lane, wv);
     for (int q = 0; q < cnt; ++q) {
-        const int jn = (q + 1 < cnt) ? (all ? q + 1 : __shfl_sync(0xffffffffu, myj, q + 1)) : j;
+        const int jn = (q + 1 < cnt) ? (all ? q + 1 : cand_at(q + 1)) : j;
         float4 wn[Q];
         load_row4<Q>(W, (unsigned)jn < (unsigned)K ? jn : 0, d4, lane, wn);   // prefetch next
         double s = warp_sum(dist_part<Q, MODE>(xv, wv));

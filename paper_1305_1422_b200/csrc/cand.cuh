@@ -3,7 +3,7 @@
 // A thread owns one data row and visits nodes j in ascending order with
 // screened values r_j.  It keeps every j with r_j <= rmin + win (rmin =
 // running minimum, win = the row's screening window).  If more than CAP
-// nodes fall inside the window, the set is cut to the CAP/2 smallest
+// nodes fall inside the window, the set is cut to the 3 CAP/4 smallest
 // (r, j) pairs in lexicographic order and a cap (capv) is installed: later
 // nodes are accepted only with r < capv (their j is larger than every held
 // index, so (r, j) < (capv, capi) <=> r < capv).  The final set is thus
@@ -88,9 +88,9 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, CandBuf b) {
     }
     s.cnt = m;
     if (m < CAP) return;
-    // Full inside the window: keep the CAP/2 smallest (value, index) pairs.
+    // Full inside the window: keep the 3 CAP / 4 smallest (value, index) pairs.
     static_assert(CAP <= 64, "keep mask is 64 bits");
-    constexpr int H = CAP / 2;
+    constexpr int H = 3 * CAP / 4;
     float capv = -INFINITY;
     unsigned long long keep = 0ull;
     for (int e = 0; e < CAP; ++e) {

@@ -37,9 +37,7 @@ constexpr int TC_BK = 64;          // fp16 features per stage (one 128B swizzle 
 constexpr int TC_UMMA_K = 16;
 constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_THREADS = 32 * (2 + TC_EPI_WARPS);
-constexpr int TC_HALF_CAP = SOMB_CAND_CAP / 2;   // candidates per (row, column group)
 constexpr int TC_ROWS = 128;                      // data rows per CTA (TMEM lanes)
-constexpr uint32_t TC_CAND_BYTES = TC_EPI_WARPS * 32 * TC_HALF_CAP * 8;
 
 // PASSES = 1: fp16 operands; PASSES = 3: split operands (hi + lo residual),
 // D += hi.hi + hi.lo + lo.hi (~22-bit operand precision, 3x the MMAs) for
@@ -51,8 +49,13 @@ struct TcCfg {
     static constexpr uint32_t A_BYTES = TC_ROWS * TC_BK * 2;       // 16 KB
     static constexpr uint32_t B_BYTES = B_ROWS * TC_BK * 2;        // 32 KB (CG 1) / 16 KB (CG 2)
     static constexpr uint32_t STAGE_BYTES = (PASSES == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
-    static constexpr int STAGES = 192 * 1024 / STAGE_BYTES;   // 6 / 4 (1-pass), 3 / 2 (3-pass)
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + TC_CAND_BYTES + 1024 + 256;
+    // candidates per (row, column group): 32 (64 per row) except the 1-CTA
+    // 3-pass variant, whose 96 KB stages leave room for 16
+    static constexpr int HALF_CAP = (CG == 1 && PASSES == 3) ? 16 : SOMB_CAND_CAP / 2;
+    static constexpr uint32_t CAND_BYTES = TC_EPI_WARPS * 32 * HALF_CAP * 8;
+    static constexpr int STAGES = (224 * 1024 - CAND_BYTES) / STAGE_BYTES;   // 5 / 3 (1-pass), 2 / 2 (3-pass)
+    static_assert(STAGES >= 2, "pipeline needs two stages");
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + CAND_BYTES + 1024 + 256;
     // kind::f16 instruction descriptor: A,B = f16, D = f32, K-major, M = 128 CG, N = 256
     static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((128 * CG) >> 4) << 24);
 };
@@ -226,8 +229,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     // stage s: A_hi at smem + s*STAGE_BYTES, B_hi after it, then A_lo, B_lo (3-pass)
     float *cbv = (float *)(smem + S * Cfg::STAGE_BYTES);
-    int *cbi = (int *)(cbv + TC_EPI_WARPS * 32 * TC_HALF_CAP);
-    uint64_t *bars = (uint64_t *)(smem + S * Cfg::STAGE_BYTES + TC_CAND_BYTES);
+    int *cbi = (int *)(cbv + TC_EPI_WARPS * 32 * Cfg::HALF_CAP);
+    uint64_t *bars = (uint64_t *)(smem + S * Cfg::STAGE_BYTES + Cfg::CAND_BYTES);
     // bars: full[S] empty[S] tfull[2] tempty[2]; then the TMEM base address
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * S + 4);
 
@@ -353,7 +356,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
         for (int u = unit0; u < num_units; u += unit_step) {
             const int64_t row = (int64_t)u * unit_rows + TC_ROWS * crank + quad * 32 + lane;
             const bool live = row < n;
-            CandRow<TC_HALF_CAP> st;
+            CandRow<Cfg::HALF_CAP> st;
             cand_init(st, live ? wcoef * xnorm[row] * nmax : 0.0f);
             if (live && thr0) st.thr = thr0[row];
             const bool dumping = dump != nullptr && live;
@@ -399,7 +402,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                             if (gmin[g8] <= st.thr) {
 #pragma unroll
                                 for (int q = 8 * g8; q < 8 * g8 + 8; ++q)
-                                    if (v[q] <= st.thr) cand_push<TC_HALF_CAP>(st, v[q], jc + q, cb);
+                                    if (v[q] <= st.thr) cand_push<Cfg::HALF_CAP>(st, v[q], jc + q, cb);
                             }
                         }
                     }
@@ -413,8 +416,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
             if (live) {
-                int *out = cand + row * SOMB_CAND_CAP + half * TC_HALF_CAP;
-                int cnt = cand_emit<TC_HALF_CAP>(st, cb, out);
+                int *out = cand + row * SOMB_CAND_CAP + half * Cfg::HALF_CAP;
+                int cnt = cand_emit<Cfg::HALF_CAP>(st, cb, out);
                 // two column groups write disjoint bytes of ccount / flags
                 reinterpret_cast<uint8_t *>(ccount + row)[half] = (uint8_t)cnt;
                 reinterpret_cast<uint8_t *>(flags + row)[half] = (uint8_t)st.trunc;
