@@ -207,7 +207,7 @@ def run_ours(args):
     K = nx * ny
     dev = torch.device("cuda", torch.cuda.current_device())
     first, count = S.partition(n, world)[rank]
-    opts = EngineOptions(screen=args.screen)
+    opts = EngineOptions(screen=args.screen, screen_passes=args.passes, rerank_order=not args.no_rerank_order)
     mtype, gtype, nb = S.MapType(mt), S.GridType(grid), S.Neighborhood(nbh)
     sparse = args.config == "cfg3"
     if sparse:
@@ -295,6 +295,7 @@ def run_ours(args):
 
     # per-phase breakdown (rank-local averages)
     phases = {k: statistics.mean(v) for k, v in phase_ms.items() if v}
+    eng.search()     # untimed: the candidate lists live in the workspace until node_sums reuses it
     cc = eng.candidate_counts()[: eng.n].float().cpu().numpy() if eng.n else np.zeros(1)
     cand_stats = {"mean": float(cc.mean()), "p50": float(np.median(cc)), "p99": float(np.percentile(cc, 99)),
                   "max": float(cc.max())}
@@ -381,6 +382,9 @@ def main():
     ap.add_argument("--screen", default="tensor", choices=["tensor", "simt", "exact"])
     ap.add_argument("--e2e-epochs", type=int, default=10)
     ap.add_argument("--ref-rows", type=int, default=0, help="CPU sample rows (0: per-config default)")
+    ap.add_argument("--passes", type=int, default=0, choices=[0, 1, 3],
+                    help="screen passes (0: auto = 3 for d <= 256)")
+    ap.add_argument("--no-rerank-order", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

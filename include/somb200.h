@@ -137,11 +137,15 @@ SOMB_API int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, cons
                                     const float *c, int32_t kp, const float *scal,
                                     float window_coef, float *dump, void *ws,
                                     void *stream);
+/* row_order (may be NULL): a permutation of [0, n) giving the order in
+ * which rows are re-ranked -- the rows sorted by their previous BMU
+ * (somb_node_sums_* row_order), so concurrently re-ranked rows share
+ * candidate codebook rows in L2.  Results do not depend on it. */
 SOMB_API int somb_bmu_rerank(const float *X, const double *x2, int64_t n,
                              int32_t d, const float *W, const double *w2,
                              int32_t K, int32_t dist_mode, int32_t screen_impl,
-                             int32_t *bmu, double *d2min, int32_t *flags,
-                             void *ws, void *stream);
+                             const int32_t *row_order, int32_t *bmu, double *d2min,
+                             int32_t *flags, void *ws, void *stream);
 
 /* qe_sum = sum_i sqrt(d2min_i) in fixed order (kernels.py:407, 427). */
 SOMB_API int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws,
@@ -153,9 +157,10 @@ SOMB_API int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws,
  * somb_hood_update this replaces the accumulate of kernels.py:225-226
  * (num = H S, den = H cnt).  ws >= somb_node_sums_ws(n, K). */
 SOMB_API size_t somb_node_sums_ws(int64_t n, int32_t d, int32_t K);
+/* row_order (may be NULL): receives the rows stably sorted by BMU. */
 SOMB_API int somb_node_sums_dense(const float *X, int64_t n, int32_t d,
                          const int32_t *bmu, int32_t K, double *S, double *cnt,
-                         void *ws, void *stream);
+                         int32_t *row_order, void *ws, void *stream);
 
 /* ---- batch update: neighbourhood convolution + blend ------------------
  * h(b, j) from grid offsets (kernels.py:99-150; hex/bubble/compact are
@@ -201,7 +206,7 @@ SOMB_API int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const fl
 SOMB_API int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col,
                                    const float *val, int64_t n, int32_t d,
                                    const int32_t *bmu, int32_t K, double *S,
-                                   double *cnt, void *ws, void *stream);
+                                   double *cnt, int32_t *row_order, void *ws, void *stream);
 
 /* Number of kernels this library has launched (process lifetime). */
 SOMB_API unsigned long long somb_launch_count(void);

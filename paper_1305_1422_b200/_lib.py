@@ -55,11 +55,11 @@ SIGNATURES = {
                                  I32, I32, P, P, P, P, P]),
     "somb_bmu_screen": (C.c_int, [P, P, P, I64, I32, P, P, P, I32, I32, P, F32, P, I32, P, P, P]),
     "somb_debug_screen_dump": (C.c_int, [P, P, P, I64, I32, P, P, P, I32, P, F32, P, P, P]),
-    "somb_bmu_rerank": (C.c_int, [P, P, I64, I32, P, P, I32, I32, I32, P, P, P, P, P]),
+    "somb_bmu_rerank": (C.c_int, [P, P, I64, I32, P, P, I32, I32, I32, P, P, P, P, P, P]),
     "somb_qe_sum": (C.c_int, [P, I64, P, P, P]),
     "somb_launch_count": (C.c_ulonglong, []),
     "somb_node_sums_ws": (SZ, [I64, I32, I32]),
-    "somb_node_sums_dense": (C.c_int, [P, I64, I32, P, I32, P, P, P, P]),
+    "somb_node_sums_dense": (C.c_int, [P, I64, I32, P, I32, P, P, P, P, P]),
     "somb_hood_ws": (SZ, [C.POINTER(SombMap), I32, I32]),
     "somb_hood_update": (C.c_int, [P, P, I32, C.POINTER(SombMap), C.POINTER(SombHood), F64, P,
                                    P, I32, I32, P, P, P, P, P]),
@@ -68,7 +68,7 @@ SIGNATURES = {
     "somb_sparse_codebook_T": (C.c_int, [P, P, I32, I32, I32, P, P]),
     "somb_bmu_sparse": (C.c_int, [P, P, P, I64, I32, P, P, P, P, I32, I32, P, P, P, F32, I32,
                                   P, P, P, P, P]),
-    "somb_node_sums_sparse": (C.c_int, [P, P, P, I64, I32, P, I32, P, P, P, P]),
+    "somb_node_sums_sparse": (C.c_int, [P, P, P, I64, I32, P, I32, P, P, P, P, P]),
     "somb_umatrix": (C.c_int, [P, I32, C.POINTER(SombMap), P, P]),
 }
 

@@ -142,11 +142,12 @@ screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __hal
 __global__ void rerank_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n,
                               int d, const float *__restrict__ W, const double *__restrict__ w2,
                               int K, const int *__restrict__ cand, const int *__restrict__ ccount,
-                              int dist_mode, int all, int split, int *__restrict__ bmu,
-                              double *__restrict__ d2min) {
-    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+                              int dist_mode, int all, int split, const int *__restrict__ order,
+                              int *__restrict__ bmu, double *__restrict__ d2min) {
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
-    if (row >= n) return;
+    if (w >= n) return;
+    const int64_t row = order ? (int64_t)order[w] : w;
     const float *x = X + row * d;
     // candidate list: one segment [0, cc) or, for the two-half tcgen05
     // epilogue, [0, cc & 255) and [CAP/2, CAP/2 + (cc >> 8 & 255))
@@ -229,10 +230,11 @@ __global__ void __launch_bounds__(256, 2)
 rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n, int d,
                   const float *__restrict__ W, const double *__restrict__ w2, int K,
                   const int *__restrict__ cand, const int *__restrict__ ccount, int split,
-                  int *__restrict__ bmu, double *__restrict__ d2min) {
-    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+                  const int *__restrict__ order, int *__restrict__ bmu, double *__restrict__ d2min) {
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
-    if (row >= n) return;
+    if (w >= n) return;
+    const int64_t row = order ? (int64_t)order[w] : w;
     const int d4 = d >> 2;
     float4 xv[Q];
     load_row4<Q>(X, row, d4, lane, xv);
@@ -281,11 +283,13 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
 template <int Q>
 static void launch_rerank_vec(unsigned blocks, cudaStream_t st, const float *X, const double *x2, int64_t n, int d,
                               const float *W, const double *w2, int K, const int *cand, const int *ccount, int mode,
-                              int split, int *bmu, double *d2min) {
+                              int split, const int *order, int *bmu, double *d2min) {
     if (mode == SOMB_DIST_NAIVE)
-        rerank_vec_kernel<Q, SOMB_DIST_NAIVE><<<blocks, 256, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, split, bmu, d2min);
+        rerank_vec_kernel<Q, SOMB_DIST_NAIVE><<<blocks, 256, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, split, order,
+                                                                       bmu, d2min);
     else
-        rerank_vec_kernel<Q, SOMB_DIST_BLOCKED><<<blocks, 256, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, split, bmu, d2min);
+        rerank_vec_kernel<Q, SOMB_DIST_BLOCKED><<<blocks, 256, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, split, order,
+                                                                         bmu, d2min);
 }
 
 // --------------------------------------------------------- qe reduction
@@ -363,7 +367,8 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
 
 extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int32_t d, const float *W,
                                const double *w2, int32_t K, int32_t dist_mode, int32_t screen_impl,
-                               int32_t *bmu, double *d2min, int32_t *flags, void *ws, void *stream) {
+                               const int32_t *row_order, int32_t *bmu, double *d2min, int32_t *flags, void *ws,
+                               void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0, SOMB_E_INPUT, "bmu_rerank: bad shape K=%d d=%d", K, d);
     SOMB_REQUIRE(dist_mode == SOMB_DIST_BLOCKED || dist_mode == SOMB_DIST_NAIVE, SOMB_E_CONFIG,
                  "bmu_rerank: bad dist_mode %d", dist_mode);
@@ -377,16 +382,16 @@ extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int3
     const unsigned blocks = (unsigned)((n + wpb - 1) / wpb);
     if (!all && d % 4 == 0 && d <= 1024) {
         if (d <= 128)
-            launch_rerank_vec<1>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, bmu, d2min);
+            launch_rerank_vec<1>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, bmu, d2min);
         else if (d <= 256)
-            launch_rerank_vec<2>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, bmu, d2min);
+            launch_rerank_vec<2>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, bmu, d2min);
         else if (d <= 512)
-            launch_rerank_vec<4>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, bmu, d2min);
+            launch_rerank_vec<4>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, bmu, d2min);
         else
-            launch_rerank_vec<8>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, bmu, d2min);
+            launch_rerank_vec<8>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, bmu, d2min);
     } else {
-        rerank_kernel<<<blocks, 32 * wpb, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, split, bmu,
-                                                   d2min);
+        rerank_kernel<<<blocks, 32 * wpb, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, split,
+                                                   row_order, bmu, d2min);
     }
     note_launch();
     SOMB_LAUNCH_CHECK("rerank");
@@ -404,7 +409,7 @@ extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *x
     int rc = somb_bmu_screen(Xh, nullptr, xnorm, n, dp, Wh, nullptr, c, K, kp, scal, window_coef, nullptr,
                              screen_impl, flags, ws, stream);
     if (rc) return rc;
-    return somb_bmu_rerank(X, x2, n, d, W, w2, K, dist_mode, screen_impl, bmu, d2min, flags, ws, stream);
+    return somb_bmu_rerank(X, x2, n, d, W, w2, K, dist_mode, screen_impl, nullptr, bmu, d2min, flags, ws, stream);
 }
 
 extern "C" int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws, void *stream) {

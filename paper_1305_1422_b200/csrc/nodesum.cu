@@ -280,7 +280,7 @@ int node_bucket_sort(const int *bmu, int64_t n, int K, void *ws, const int **per
 }  // namespace somb
 
 extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const int32_t *bmu, int32_t K,
-                                    double *S, double *cnt, void *ws, void *stream) {
+                                    double *S, double *cnt, int32_t *row_order, void *ws, void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0 && n >= 0 && n < (1ll << 31), SOMB_E_INPUT,
                  "node_sums: bad shape n=%lld d=%d K=%d", (long long)n, d, K);
     cudaStream_t st = as_stream(stream);
@@ -289,6 +289,7 @@ extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const 
     const int *perm = nullptr, *off = nullptr;
     int rc = node_bucket_sort(bmu, n, K, ws, &perm, &off, cnt, st);
     if (rc || n == 0) return rc;
+    if (row_order) cudaMemcpyAsync(row_order, perm, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, st);
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.nseg, K, w.segoff);
     note_launch();
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.mseg, K, w.msegoff);

@@ -221,8 +221,8 @@ extern "C" int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const 
 }
 
 extern "C" int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col, const float *val, int64_t n,
-                                     int32_t d, const int32_t *bmu, int32_t K, double *S, double *cnt, void *ws,
-                                     void *stream) {
+                                     int32_t d, const int32_t *bmu, int32_t K, double *S, double *cnt,
+                                     int32_t *row_order, void *ws, void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0 && n < (1ll << 31), SOMB_E_INPUT, "node_sums_sparse: bad shape");
     cudaStream_t st = as_stream(stream);
     cudaMemsetAsync(S, 0, (size_t)K * d * sizeof(double), st);
@@ -230,6 +230,7 @@ extern "C" int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col, 
     int rc = node_bucket_sort(bmu, n, K, ws, &perm, &off, cnt, st);
     if (rc) return rc;
     if (n == 0) return SOMB_OK;
+    if (row_order) cudaMemcpyAsync(row_order, perm, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, st);
     sp_node_sums_kernel<<<K, 256, 0, st>>>(rowptr, col, val, d, perm, off, K, S);
     note_launch();
     SOMB_LAUNCH_CHECK("node_sums_sparse");

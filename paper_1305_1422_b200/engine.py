@@ -42,6 +42,7 @@ class EngineOptions:
     screen_passes: int = 0            # 0 auto (3 if the padded feature count <= 256), 1, or 3
     window_kappa3: Optional[float] = None     # None: _kappa3(d)
     conv: str = "auto"                # neighbourhood convolution: "auto", "direct", "spectral"
+    rerank_order: bool = True         # re-rank rows in previous-BMU order (L2 locality; same result)
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -112,6 +113,10 @@ class SomEngine:
         self.bmu = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         self.d2min = torch.empty(max(n, 1), dtype=f64, device=dev)
         self.flags = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        # rows sorted by BMU (written by node_sums): the next re-rank visits rows
+        # in this order so concurrently re-ranked rows share codebook rows in L2
+        self.row_order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.has_order = False
         # packed [S (K*d) | cnt (K) | qe (1)] fp64: one all-reduce per epoch
         self.acc = torch.zeros(self.K * d + self.K + 1, dtype=f64, device=dev)
         self.S = self.acc[: self.K * d].view(self.K, d)
@@ -231,7 +236,8 @@ class SomEngine:
         self._mark("screen", False)
         self._mark("rerank", True)
         _lib.call("somb_bmu_rerank", _ptr(self.X), _ptr(self.x2), self.n, self.d, _ptr(self.W),
-                  _ptr(self.w2), self.K, dist_mode, self.screen_impl, _ptr(self.bmu),
+                  _ptr(self.w2), self.K, dist_mode, self.screen_impl,
+                  _ptr(self.row_order if (self.has_order and self.opt.rerank_order) else None), _ptr(self.bmu),
                   _ptr(self.d2min), _ptr(self.flags), _ptr(self.ws), st)
         self._mark("rerank", False)
         self.has_prev = True
@@ -261,7 +267,8 @@ class SomEngine:
 
     def node_sums(self):
         _lib.call("somb_node_sums_dense", _ptr(self.X), self.n, self.d, _ptr(self.bmu), self.K,
-                  _ptr(self.S), _ptr(self.cnt), _ptr(self.ws), _stream(self.dev))
+                  _ptr(self.S), _ptr(self.cnt), _ptr(self.row_order), _ptr(self.ws), _stream(self.dev))
+        self.has_order = True
 
     def reduce(self):
         if self.world > 1:
