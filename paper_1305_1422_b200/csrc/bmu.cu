@@ -12,7 +12,8 @@ namespace somb {
 int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh,
                      const __half *Wl, int kp, const float *c, const float *xnorm, const float *scal,
                      float wcoef, const float *thr0, int *cand, int *ccount, int *flags, float *dump,
-                     cudaStream_t st);
+                     void *scratch, cudaStream_t st);
+size_t screen_tc_scratch_bytes();
 
 // Seed of each row's acceptance threshold from its previous BMU: the screened
 // value of that node (same fp16 operands, fp32 FMA) plus one window and an
@@ -329,10 +330,11 @@ __global__ void qe_final(const double *__restrict__ part, int np, double *__rest
 
 using namespace somb;
 
-// ws layout: cand [n][CAP] int | ccount [n] int | thr0 [n] float
-extern "C" size_t somb_bmu_ws(int64_t n) {
+// ws layout: cand [n][CAP] int | ccount [n] int | thr0 [n] float | screen scratch
+static size_t bmu_ws_fixed(int64_t n) {
     return align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256) + 2 * align_up((size_t)n * sizeof(int), 256);
 }
+extern "C" size_t somb_bmu_ws(int64_t n) { return bmu_ws_fixed(n) + screen_tc_scratch_bytes(); }
 
 extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm, int64_t n, int32_t dp,
                                const uint16_t *Wh, const uint16_t *Wl, const float *c, int32_t K, int32_t kp,
@@ -356,7 +358,7 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
     if (screen_impl == 0)
         return launch_screen_tc((const __half *)Xh, (const __half *)Xl, n, dp, (const __half *)Wh,
                                 (const __half *)Wl, kp, c, xnorm, scal, window_coef, thr0, cand, ccount, flags,
-                                nullptr, st);
+                                nullptr, (char *)ws + bmu_ws_fixed(n), st);
     unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
     screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh, kp, c,
                                                       xnorm, scal, window_coef, thr0, cand, ccount, flags);
@@ -439,5 +441,6 @@ extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, co
     int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
     int *flags = (int *)((char *)ccount + align_up((size_t)n * sizeof(int), 256));
     return launch_screen_tc((const __half *)Xh, (const __half *)Xl, m, dp, (const __half *)Wh, (const __half *)Wl, kp,
-                            c, xnorm, scal, window_coef, nullptr, cand, ccount, flags, dump, as_stream(stream));
+                            c, xnorm, scal, window_coef, nullptr, cand, ccount, flags, dump,
+                            (char *)ws + bmu_ws_fixed(n), as_stream(stream));
 }

@@ -48,6 +48,12 @@ struct CandBuf {
     uint32_t v, i;      // shared addresses of this thread's slot 0 (values, indices)
     uint32_t stride;    // bytes between slots
 };
+__device__ __forceinline__ float cb_ldv(const CandBuf &b, int e) { return lds_f32(b.v + e * b.stride); }
+__device__ __forceinline__ int cb_ldi(const CandBuf &b, int e) { return lds_s32(b.i + e * b.stride); }
+__device__ __forceinline__ void cb_st(const CandBuf &b, int e, float v, int j) {
+    sts_f32(b.v + e * b.stride, v);
+    sts_s32(b.i + e * b.stride, j);
+}
 
 template <int CAP>
 struct CandRow {
@@ -73,16 +79,15 @@ __device__ __forceinline__ void cand_bound(CandRow<CAP> &s, float r_seen) {
     s.thr = fminf(s.thr, r_seen + s.win);
 }
 
-template <int CAP>
-__device__ __noinline__ void cand_make_room(CandRow<CAP> &s, CandBuf b) {
+template <int CAP, class Buf>
+__device__ __noinline__ void cand_make_room(CandRow<CAP> &s, Buf b) {
     const float lim = s.rmin + s.win;
     int m = 0;
     for (int e = 0; e < s.cnt; ++e) {
-        float v = lds_f32(b.v + e * b.stride);
-        int ix = lds_s32(b.i + e * b.stride);
+        float v = cb_ldv(b, e);
+        int ix = cb_ldi(b, e);
         if (v <= lim) {
-            sts_f32(b.v + m * b.stride, v);
-            sts_s32(b.i + m * b.stride, ix);
+            cb_st(b, m, v, ix);
             ++m;
         }
     }
@@ -94,12 +99,12 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, CandBuf b) {
     float capv = -INFINITY;
     unsigned long long keep = 0ull;
     for (int e = 0; e < CAP; ++e) {
-        float v = lds_f32(b.v + e * b.stride);
-        int ix = lds_s32(b.i + e * b.stride);
+        float v = cb_ldv(b, e);
+        int ix = cb_ldi(b, e);
         int rank = 0;
         for (int f = 0; f < CAP; ++f) {
-            float u = lds_f32(b.v + f * b.stride);
-            int iu = lds_s32(b.i + f * b.stride);
+            float u = cb_ldv(b, f);
+            int iu = cb_ldi(b, f);
             rank += (u < v) || (u == v && iu < ix);
         }
         if (rank < H) {
@@ -110,8 +115,7 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, CandBuf b) {
     m = 0;
     for (int e = 0; e < CAP; ++e) {
         if (keep >> e & 1ull) {
-            sts_f32(b.v + m * b.stride, lds_f32(b.v + e * b.stride));
-            sts_s32(b.i + m * b.stride, lds_s32(b.i + e * b.stride));
+            cb_st(b, m, cb_ldv(b, e), cb_ldi(b, e));
             ++m;
         }
     }
@@ -121,8 +125,8 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, CandBuf b) {
     s.thr = fminf(s.thr, s.capbelow);
 }
 
-template <int CAP>
-__device__ __forceinline__ void cand_push(CandRow<CAP> &s, float r, int j, CandBuf b) {
+template <int CAP, class Buf>
+__device__ __forceinline__ void cand_push(CandRow<CAP> &s, float r, int j, const Buf &b) {
     if (r <= s.thr) {
         if (r < s.rmin) {
             s.rmin = r;
@@ -130,20 +134,19 @@ __device__ __forceinline__ void cand_push(CandRow<CAP> &s, float r, int j, CandB
         }
         if (s.cnt == CAP) cand_make_room<CAP>(s, b);
         if (r <= s.thr) {
-            sts_f32(b.v + s.cnt * b.stride, r);
-            sts_s32(b.i + s.cnt * b.stride, j);
+            cb_st(b, s.cnt, r, j);
             ++s.cnt;
         }
     }
 }
 
 // Final filter: write { held j : r_j <= rmin + win } in index order.
-template <int CAP>
-__device__ __forceinline__ int cand_emit(const CandRow<CAP> &s, CandBuf b, int *out) {
+template <int CAP, class Buf>
+__device__ __forceinline__ int cand_emit(const CandRow<CAP> &s, const Buf &b, int *out) {
     const float lim = s.rmin + s.win;
     int m = 0;
     for (int e = 0; e < s.cnt; ++e)
-        if (lds_f32(b.v + e * b.stride) <= lim) out[m++] = lds_s32(b.i + e * b.stride);
+        if (cb_ldv(b, e) <= lim) out[m++] = cb_ldi(b, e);
     return m;
 }
 

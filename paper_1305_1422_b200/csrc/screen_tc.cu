@@ -28,6 +28,8 @@
 // sweep and is written out once.
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "cand.cuh"
 
 namespace somb {
@@ -43,17 +45,20 @@ constexpr int TC_ROWS = 128;                      // data rows per CTA (TMEM lan
 // D += hi.hi + hi.lo + lo.hi (~22-bit operand precision, 3x the MMAs) for
 // small feature counts where the 1-pass fp16 window holds too many
 // near-tied nodes.  A stage holds [A_hi | B_hi | A_lo | B_lo].
-template <int CG, int PASSES = 1>
+template <int CG, int PASSES = 1, int HC = SOMB_CAND_CAP / 2>
 struct TcCfg {
     static constexpr int B_ROWS = TC_BN / CG;                      // codebook rows loaded per CTA
     static constexpr uint32_t A_BYTES = TC_ROWS * TC_BK * 2;       // 16 KB
     static constexpr uint32_t B_BYTES = B_ROWS * TC_BK * 2;        // 32 KB (CG 1) / 16 KB (CG 2)
     static constexpr uint32_t STAGE_BYTES = (PASSES == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
-    // candidates per (row, column group): 32 (64 per row) except the 1-CTA
-    // 3-pass variant, whose 96 KB stages leave room for 16
-    static constexpr int HALF_CAP = (CG == 1 && PASSES == 3) ? 16 : SOMB_CAND_CAP / 2;
+    // candidates kept per (row, column group): HC (<= SOMB_CAND_CAP / 2) in
+    // shared memory; when a group's window holds more, its 3 HC / 4 lowest
+    // screened (value, index) pairs are kept (cand.cuh)
+    static constexpr int HALF_CAP = HC;
+    static_assert(HC <= SOMB_CAND_CAP / 2, "column-group capacity exceeds the candidate list");
     static constexpr uint32_t CAND_BYTES = TC_EPI_WARPS * 32 * HALF_CAP * 8;
-    static constexpr int STAGES = (224 * 1024 - CAND_BYTES) / STAGE_BYTES;   // 5 / 3 (1-pass), 2 / 2 (3-pass)
+    static constexpr int STAGES_RAW = (224 * 1024 - CAND_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static_assert(STAGES >= 2, "pipeline needs two stages");
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + CAND_BYTES + 1024 + 256;
     // kind::f16 instruction descriptor: A,B = f16, D = f32, K-major, M = 128 CG, N = 256
@@ -215,15 +220,16 @@ __constant__ int g_profile_mode = 0;
 __constant__ int g_a_evict_last = 0;
 
 // ------------------------------------------------------------------ kernel
-template <int CG, int PASSES>
+template <int CG, int PASSES, int HC>
 __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const CUtensorMap *map_w,
                                                const CUtensorMap *map_xl, const CUtensorMap *map_wl, int64_t n,
                                                int dp, int kp, const float *__restrict__ c,
                                                const float *__restrict__ xnorm, const float *__restrict__ scal,
                                                float wcoef, const float *__restrict__ thr0, int *__restrict__ cand,
                                                int *__restrict__ ccount, int *__restrict__ flags,
-                                               float *__restrict__ dump) {
-    using Cfg = TcCfg<CG, PASSES>;
+                                               float *__restrict__ dump, unsigned *__restrict__ sync_ctr,
+                                               int lag) {
+    using Cfg = TcCfg<CG, PASSES, HC>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -281,9 +287,24 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             const bool hint_a = g_a_evict_last != 0;
             int stage = 0;
             uint32_t phase = 0;
+            // soft lockstep (lag > 0): a CTA starts its g-th node tile only once
+            // all CTAs together have issued P * (g - lag) tiles, so concurrent
+            // CTAs sweep the same codebook tiles and share them in L2
+            const unsigned P = gridDim.x;
+            const int waves = (num_units + unit_step - 1) / unit_step;
+            unsigned issued = 0;
             for (int u = unit0; u < num_units; u += unit_step) {
                 const int row0 = u * unit_rows + TC_ROWS * (int)crank;
                 for (int nt = 0; nt < NT; ++nt) {
+                    if (lag > 0 && issued > (unsigned)lag) {
+                        const unsigned need = P * (issued - (unsigned)lag);
+                        for (int spin = 0; spin < (1 << 20); ++spin) {
+                            unsigned cur;
+                            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(sync_ctr) : "memory");
+                            if (cur >= need) break;
+                            __nanosleep(64);
+                        }
+                    }
                     const int node0 = nt * TC_BN + Cfg::B_ROWS * (int)crank;
                     for (int kb = 0; kb < KB; ++kb) {
                         mbar_wait(empty0 + 8 * stage, phase ^ 1);
@@ -302,7 +323,14 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         }
                         if (++stage == S) { stage = 0; phase ^= 1; }
                     }
+                    ++issued;
+                    if (lag > 0) atomicAdd(sync_ctr, 1u);
                 }
+            }
+            // CTAs with fewer waves credit their missing tiles so nobody waits on them
+            if (lag > 0) {
+                const unsigned total = (unsigned)waves * (unsigned)NT;
+                if (total > issued) atomicAdd(sync_ctr, total - issued);
             }
         }
     } else if (warp == 1) {
@@ -416,7 +444,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
             if (live) {
-                int *out = cand + row * SOMB_CAND_CAP + half * Cfg::HALF_CAP;
+                int *out = cand + row * SOMB_CAND_CAP + half * (SOMB_CAND_CAP / 2);
                 int cnt = cand_emit<Cfg::HALF_CAP>(st, cb, out);
                 // two column groups write disjoint bytes of ccount / flags
                 reinterpret_cast<uint8_t *>(ccount + row)[half] = (uint8_t)cnt;
@@ -441,18 +469,18 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
         const __grid_constant__ CUtensorMap map_xl, const __grid_constant__ CUtensorMap map_wl, int64_t n, int dp, int kp, \
         const float *__restrict__ c, const float *__restrict__ xnorm, const float *__restrict__ scal, float wcoef,  \
         const float *__restrict__ thr0, int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags,  \
-        float *__restrict__ dump
+        float *__restrict__ dump, unsigned *__restrict__ sync_ctr, int lag
 
-template <int P>
+template <int P, int HC>
 __global__ void __launch_bounds__(TC_THREADS, 1) screen_tc1_kernel(SCREEN_TC_ARGS) {
-    screen_tc_body<1, P>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount, flags,
-                         dump);
+    screen_tc_body<1, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
+                             flags, dump, sync_ctr, lag);
 }
 
-template <int P>
+template <int P, int HC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) screen_tc2_kernel(SCREEN_TC_ARGS) {
-    screen_tc_body<2, P>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount, flags,
-                         dump);
+    screen_tc_body<2, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
+                             flags, dump, sync_ctr, lag);
 }
 
 // --------------------------------------------------------------- host side
@@ -487,6 +515,8 @@ static int make_map(CUtensorMap *map, const void *base, uint64_t inner, uint64_t
 }
 
 static int g_tc_group = 2;   // SOMB_TC_GROUP=1 selects the single-CTA variant (A/B testing)
+static int g_half_cap = 32;  // SOMB_HALF_CAP = 8 | 16 | 32: candidates kept per (row, column group)
+static int g_lag = 8;        // SOMB_SCREEN_LAG: soft lockstep of the CTAs' codebook sweeps (0 = off)
 
 template <class KernelT>
 static int set_smem(KernelT k, uint32_t bytes, const char *what) {
@@ -494,24 +524,34 @@ static int set_smem(KernelT k, uint32_t bytes, const char *what) {
     return r == cudaSuccess ? SOMB_OK : cuda_status(r, what);
 }
 
+size_t screen_tc_scratch_bytes() { return 256; }   // the lockstep counter
+
 int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh, const __half *Wl, int kp,
                      const float *c, const float *xnorm, const float *scal, float wcoef, const float *thr0, int *cand,
-                     int *ccount, int *flags, float *dump, cudaStream_t st) {
+                     int *ccount, int *flags, float *dump, void *scratch, cudaStream_t st) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % TC_BN == 0, SOMB_E_INPUT, "screen_tc: dp %% 8 and kp %% 256 required");
     static bool init = false;
     if (!init) {
         const char *e = getenv("SOMB_TC_GROUP");
         if (e && atoi(e) == 1) g_tc_group = 1;
+        const char *hc = getenv("SOMB_HALF_CAP");
+        if (hc) g_half_cap = atoi(hc) <= 8 ? 8 : atoi(hc) <= 16 ? 16 : 32;
+        const char *lg = getenv("SOMB_SCREEN_LAG");
+        if (lg) g_lag = atoi(lg);
         const char *pm = getenv("SOMB_SCREEN_PROFILE");
         int mode = pm ? atoi(pm) : 0;
         cudaMemcpyToSymbol(g_profile_mode, &mode, sizeof(int));
         const char *ae = getenv("SOMB_A_EVICT_LAST");
         int a_last = ae ? atoi(ae) : 0;
         cudaMemcpyToSymbol(g_a_evict_last, &a_last, sizeof(int));
-        int rc = set_smem(screen_tc1_kernel<1>, TcCfg<1, 1>::SMEM, "screen_tc1 smem");
-        if (!rc) rc = set_smem(screen_tc2_kernel<1>, TcCfg<2, 1>::SMEM, "screen_tc2 smem");
-        if (!rc) rc = set_smem(screen_tc1_kernel<3>, TcCfg<1, 3>::SMEM, "screen_tc1x3 smem");
-        if (!rc) rc = set_smem(screen_tc2_kernel<3>, TcCfg<2, 3>::SMEM, "screen_tc2x3 smem");
+        int rc = set_smem(screen_tc1_kernel<1, 16>, TcCfg<1, 1, 16>::SMEM, "screen_tc1 smem");
+        if (!rc) rc = set_smem(screen_tc1_kernel<3, 16>, TcCfg<1, 3, 16>::SMEM, "screen_tc1x3 smem");
+        if (!rc) rc = set_smem(screen_tc2_kernel<1, 8>, TcCfg<2, 1, 8>::SMEM, "screen_tc2 smem");
+        if (!rc) rc = set_smem(screen_tc2_kernel<1, 16>, TcCfg<2, 1, 16>::SMEM, "screen_tc2 smem");
+        if (!rc) rc = set_smem(screen_tc2_kernel<1, 32>, TcCfg<2, 1, 32>::SMEM, "screen_tc2 smem");
+        if (!rc) rc = set_smem(screen_tc2_kernel<3, 8>, TcCfg<2, 3, 8>::SMEM, "screen_tc2x3 smem");
+        if (!rc) rc = set_smem(screen_tc2_kernel<3, 16>, TcCfg<2, 3, 16>::SMEM, "screen_tc2x3 smem");
+        if (!rc) rc = set_smem(screen_tc2_kernel<3, 32>, TcCfg<2, 3, 32>::SMEM, "screen_tc2x3 smem");
         if (rc) return rc;
         init = true;
     }
@@ -528,16 +568,25 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaMemsetAsync(ccount, 0, (size_t)n * sizeof(int), st);
     cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
+    unsigned *ctr = (unsigned *)scratch;
+    const int lag = g_lag;
+    if (lag > 0) cudaMemsetAsync(ctr, 0, sizeof(unsigned), st);
     const int units = (int)((n + TC_ROWS * cg - 1) / (TC_ROWS * cg));
     const int max_units = sms / cg;
     const int grid = cg * (units < max_units ? units : max_units);
-#define SCREEN_LAUNCH(KERN, CGV, PV)                                                                                  \
-    KERN<PV><<<grid, TC_THREADS, TcCfg<CGV, PV>::SMEM, st>>>(mx, mw, mxl, mwl, n, dp, kp, c, xnorm, scal, wcoef, thr0, \
-                                                             cand, ccount, flags, dump)
-    if (cg == 2) {
-        if (three) SCREEN_LAUNCH(screen_tc2_kernel, 2, 3); else SCREEN_LAUNCH(screen_tc2_kernel, 2, 1);
+#define SCREEN_LAUNCH(KERN, CGV, PV, HV)                                                                            \
+    KERN<PV, HV><<<grid, TC_THREADS, TcCfg<CGV, PV, HV>::SMEM, st>>>(mx, mw, mxl, mwl, n, dp, kp, c, xnorm, scal, wcoef, \
+                                                                     thr0, cand, ccount, flags, dump, ctr, lag)
+    if (cg == 1) {
+        if (three) SCREEN_LAUNCH(screen_tc1_kernel, 1, 3, 16); else SCREEN_LAUNCH(screen_tc1_kernel, 1, 1, 16);
+    } else if (three) {
+        if (g_half_cap == 8) SCREEN_LAUNCH(screen_tc2_kernel, 2, 3, 8);
+        else if (g_half_cap == 16) SCREEN_LAUNCH(screen_tc2_kernel, 2, 3, 16);
+        else SCREEN_LAUNCH(screen_tc2_kernel, 2, 3, 32);
     } else {
-        if (three) SCREEN_LAUNCH(screen_tc1_kernel, 1, 3); else SCREEN_LAUNCH(screen_tc1_kernel, 1, 1);
+        if (g_half_cap == 8) SCREEN_LAUNCH(screen_tc2_kernel, 2, 1, 8);
+        else if (g_half_cap == 16) SCREEN_LAUNCH(screen_tc2_kernel, 2, 1, 16);
+        else SCREEN_LAUNCH(screen_tc2_kernel, 2, 1, 32);
     }
 #undef SCREEN_LAUNCH
     note_launch();

@@ -51,3 +51,6 @@ for e in range(10):
     print(json.dumps(row), flush=True)
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 json.dump(rows, open(os.path.join(ROOT, "gpurun_out", f"epoch_profile_{cfg}_p{eng.passes}.json"), "w"), indent=1)
+w = eng.W[: eng.K].double()
+print(json.dumps({"codebook_sum": float(w.sum()), "codebook_sq": float((w * w).sum()),
+                  "bmu_hash": int((eng.bmu[: eng.n].long() * torch.arange(1, eng.n + 1, device=dev)).sum())}))

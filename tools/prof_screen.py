@@ -1,5 +1,7 @@
-"""Profile helper: one cfg-shaped BMU search (screen + re-rank) on cuda:0.
-   python tools/prof_screen.py [rows] [d] [nx] [ny] [reps]"""
+"""Profile helper: cfg-shaped BMU searches (screen + re-rank) on cuda:0 after
+`warm` training epochs of the reference schedule (epochs 2-7 of cfg2 are the
+candidate-heavy regime).
+   python tools/prof_screen.py [rows] [d] [nx] [ny] [reps] [warm_epochs]"""
 import os
 import sys
 
@@ -14,19 +16,19 @@ d = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
 nx = int(sys.argv[3]) if len(sys.argv) > 3 else 200
 ny = int(sys.argv[4]) if len(sys.argv) > 4 else 200
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 2
+warm = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 g = torch.Generator(device="cuda")
 g.manual_seed(1001)
 X = torch.rand((n, d), generator=g, device="cuda")
 eng = SomEngine(X, nx, ny, S.MapType.TOROID)
 eng.set_codebook(S.init_codebook(S.TrainConfig(n_columns=nx, n_rows=ny), d).weights)
-eng.epoch(nx / 2, 1.0, 1e-3)          # collapse the codebook like a real run
+r0 = max(min(nx, ny) / 2, 1.0)
+for e in range(warm):     # reference linear schedule, 10 epochs
+    f = e / 9
+    eng.epoch(r0 + (1 - r0) * f, 1 + (0.01 - 1) * f, 1e-3)
 for _ in range(reps):
     eng.search()
 torch.cuda.synchronize()
-cc = eng.ws[: 0].new_empty(0)
-off = ((n * 32 * 4 + 255) // 256) * 256
-cnt = eng.ws[off: off + 4 * n].view(torch.int32).cpu()
-c0, c1 = cnt & 255, (cnt >> 8) & 255
-tot = (c0 + c1).float()
+tot = eng.candidate_counts()[:n].float()
 print(f"candidates/row mean {tot.mean():.2f} p50 {tot.median():.0f} max {tot.max():.0f}; "
-      f"truncated rows {((eng.flags[:n].cpu() & 0xFFFF) != 0).float().mean():.3f}")
+      f"truncated rows {((eng.flags[:n] & 0xFFFF) != 0).float().mean():.3f}")
