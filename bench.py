@@ -300,7 +300,8 @@ def run_ours(args):
     cand_stats = {"mean": float(cc.mean()), "p50": float(np.median(cc)), "p99": float(np.percentile(cc, 99)),
                   "max": float(cc.max())}
     flags = eng.flags[: eng.n].cpu().numpy()
-    trunc = float(((flags & 0xFF) | ((flags >> 8) & 0xFF)).astype(bool).mean()) if eng.n else 0.0
+    trunc = float((((flags & 0xFF) | ((flags >> 8) & 0xFF)) & 1).astype(bool).mean()) if eng.n else 0.0
+    spilled = float((((flags & 0xFF) | ((flags >> 8) & 0xFF)) & 2).astype(bool).mean()) if eng.n else 0.0
 
     # end to end through the public API: host (pinned) data -> train() -> host results
     e2e = None
@@ -362,7 +363,7 @@ def run_ours(args):
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
                 "gpu_launches": int(launches),
                 "phase_ms": phases, "epoch_ms": ms_step,
-                "nkd_per_s": value * d, "window_truncated_rows": trunc,
+                "nkd_per_s": value * d, "window_truncated_rows": trunc, "window_spilled_rows": spilled,
                 "candidates_per_row": cand_stats}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -12,8 +12,49 @@ namespace somb {
 int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh,
                      const __half *Wl, int kp, const float *c, const float *xnorm, const float *scal,
                      float wcoef, const float *thr0, int *cand, int *ccount, int *flags, float *dump,
-                     void *scratch, cudaStream_t st);
-size_t screen_tc_scratch_bytes();
+                     unsigned *ctrs, OvfPool pool, int *ovf_head, float *ovf_lim, cudaStream_t st);
+
+// BMU workspace: cand [n][CAP] int | ccount [n] int | thr0 [n] float |
+// counters | overflow: head [2n] int, lim [2n] float, next [C], cnt [C],
+// entries [C][32] int2 with C = max(4096, n / 4) chunks.
+struct BmuWs {
+    int *cand, *ccount;
+    float *thr0;
+    unsigned *ctrs;
+    int *ovf_head;
+    float *ovf_lim;
+    OvfPool pool;
+};
+
+static unsigned ovf_chunks(int64_t n) { return (unsigned)(n / 4 > 4096 ? n / 4 : 4096); }
+
+static BmuWs bmu_carve(void *ws, int64_t n, size_t *total = nullptr) {
+    BmuWs w;
+    char *p = (char *)ws;
+    auto take = [&](size_t bytes) { char *r = p; p += align_up(bytes, 256); return r; };
+    const unsigned C = ovf_chunks(n);
+    w.cand = (int *)take((size_t)n * SOMB_CAND_CAP * sizeof(int));
+    w.ccount = (int *)take((size_t)n * sizeof(int));
+    w.thr0 = (float *)take((size_t)n * sizeof(float));
+    w.ctrs = (unsigned *)take(4 * sizeof(unsigned));
+    w.ovf_head = (int *)take((size_t)2 * n * sizeof(int));
+    w.ovf_lim = (float *)take((size_t)2 * n * sizeof(float));
+    w.pool.next = (int *)take((size_t)C * sizeof(int));
+    w.pool.cnt = (int *)take((size_t)C * sizeof(int));
+    w.pool.ent = (int2 *)take((size_t)C * kOvfChunk * sizeof(int2));
+    w.pool.ctr = w.ctrs + 1;
+    w.pool.nchunks = C;
+    if (total) *total = (size_t)(p - (char *)ws);
+    return w;
+}
+
+// Spilled candidates of one row (tcgen05 screen overflow lists), read by the re-rank.
+struct OvfView {
+    const int *head;    // [2n], nullptr = no overflow lists
+    const float *lim;   // [2n] final window limit of each column group
+    const int2 *ent;
+    const int *next, *cnt;
+};
 
 // Seed of each row's acceptance threshold from its previous BMU: the screened
 // value of that node (same fp16 operands, fp32 FMA) plus one window and an
@@ -144,7 +185,7 @@ __global__ void rerank_kernel(const float *__restrict__ X, const double *__restr
                               int d, const float *__restrict__ W, const double *__restrict__ w2,
                               int K, const int *__restrict__ cand, const int *__restrict__ ccount,
                               int dist_mode, int all, int split, const int *__restrict__ order,
-                              int *__restrict__ bmu, double *__restrict__ d2min) {
+                              OvfView ov, int *__restrict__ bmu, double *__restrict__ d2min) {
     const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (w >= n) return;
@@ -161,8 +202,29 @@ __global__ void rerank_kernel(const float *__restrict__ X, const double *__restr
     double best = INFINITY;
     int bestj = 0x7fffffff;
     const double xx = x2[row];
-    for (int q = 0; q < cnt; ++q) {
-        int j = scan_all ? q : cand[row * SOMB_CAND_CAP + (q < c0 ? q : SOMB_CAND_CAP / 2 + (q - c0))];
+    // main list, then (tcgen05 overflow) the spilled chunks of both column groups
+    int ovh = -2, ovc = -1;      // current overflow group / chunk
+    unsigned ovbal = 0u;
+    int2 ove = make_int2(0, -1);
+    for (int q = 0;; ++q) {
+        int j;
+        if (q < cnt) {
+            j = scan_all ? q : cand[row * SOMB_CAND_CAP + (q < c0 ? q : SOMB_CAND_CAP / 2 + (q - c0))];
+        } else {
+            if (scan_all || ov.head == nullptr) break;
+            while (ovbal == 0u) {     // next chunk with in-window entries
+                if (ovc >= 0) ovc = ov.next[ovc];
+                while (ovc < 0 && ovh < 1) { ++ovh; if (ovh >= 0) ovc = ov.head[2 * row + ovh]; }
+                if (ovc < 0) break;
+                const int m = ov.cnt[ovc];
+                ove = lane < m ? ov.ent[(size_t)ovc * kOvfChunk + lane] : make_int2(0x7f800000, -1);
+                ovbal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(ove.x) <= ov.lim[2 * row + ovh]);
+            }
+            if (ovbal == 0u) break;
+            const int src = __ffs(ovbal) - 1;
+            ovbal &= ovbal - 1u;
+            j = __shfl_sync(0xffffffffu, ove.y, src);
+        }
         if ((unsigned)j >= (unsigned)K) continue;
         const float *w = W + (int64_t)j * d;
         double d2;
@@ -231,7 +293,7 @@ __global__ void __launch_bounds__(256, 2)
 rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n, int d,
                   const float *__restrict__ W, const double *__restrict__ w2, int K,
                   const int *__restrict__ cand, const int *__restrict__ ccount, int split,
-                  const int *__restrict__ order, int *__restrict__ bmu, double *__restrict__ d2min) {
+                  const int *__restrict__ order, OvfView ov, int *__restrict__ bmu, double *__restrict__ d2min) {
     const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (w >= n) return;
@@ -275,6 +337,32 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
 #pragma unroll
         for (int t = 0; t < Q; ++t) wv[t] = wn[t];
     }
+    if (ov.head != nullptr && !all) {   // spilled candidates of both column groups
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const float lim = ov.lim[2 * row + h];
+#pragma unroll 1
+            for (int c = ov.head[2 * row + h]; c >= 0; c = ov.next[c]) {
+                const int m = ov.cnt[c];
+                const int2 e = lane < m ? ov.ent[(size_t)c * kOvfChunk + lane] : make_int2(0x7f800000, -1);
+                unsigned bal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(e.x) <= lim);
+                while (bal) {
+                    const int src = __ffs(bal) - 1;
+                    bal &= bal - 1u;
+                    const int jj = __shfl_sync(0xffffffffu, e.y, src);
+                    if ((unsigned)jj >= (unsigned)K) continue;
+                    load_row4<Q>(W, jj, d4, lane, wv);
+                    double sd = warp_sum(dist_part<Q, MODE>(xv, wv));
+                    double v = sd;
+                    if (MODE == SOMB_DIST_BLOCKED) v = fmax(__dadd_rn(__dadd_rn(__dmul_rn(-2.0, sd), xx), w2[jj]), 0.0);
+                    if (v < best || (v == best && jj < bestj)) {
+                        best = v;
+                        bestj = jj;
+                    }
+                }
+            }
+        }
+    }
     if (lane == 0) {
         bmu[row] = bestj;
         d2min[row] = best;
@@ -284,13 +372,13 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
 template <int Q>
 static void launch_rerank_vec(unsigned blocks, cudaStream_t st, const float *X, const double *x2, int64_t n, int d,
                               const float *W, const double *w2, int K, const int *cand, const int *ccount, int mode,
-                              int split, const int *order, int *bmu, double *d2min) {
+                              int split, const int *order, OvfView ov, int *bmu, double *d2min) {
     if (mode == SOMB_DIST_NAIVE)
         rerank_vec_kernel<Q, SOMB_DIST_NAIVE><<<blocks, 256, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, split, order,
-                                                                       bmu, d2min);
+                                                                       ov, bmu, d2min);
     else
         rerank_vec_kernel<Q, SOMB_DIST_BLOCKED><<<blocks, 256, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, split, order,
-                                                                         bmu, d2min);
+                                                                         ov, bmu, d2min);
 }
 
 // --------------------------------------------------------- qe reduction
@@ -330,11 +418,11 @@ __global__ void qe_final(const double *__restrict__ part, int np, double *__rest
 
 using namespace somb;
 
-// ws layout: cand [n][CAP] int | ccount [n] int | thr0 [n] float | screen scratch
-static size_t bmu_ws_fixed(int64_t n) {
-    return align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256) + 2 * align_up((size_t)n * sizeof(int), 256);
+extern "C" size_t somb_bmu_ws(int64_t n) {
+    size_t total = 0;
+    bmu_carve(nullptr, n, &total);
+    return total + 256;
 }
-extern "C" size_t somb_bmu_ws(int64_t n) { return bmu_ws_fixed(n) + screen_tc_scratch_bytes(); }
 
 extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm, int64_t n, int32_t dp,
                                const uint16_t *Wh, const uint16_t *Wl, const float *c, int32_t K, int32_t kp,
@@ -344,11 +432,11 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
     SOMB_REQUIRE(screen_impl >= 0 && screen_impl <= 2, SOMB_E_CONFIG, "bad screen_impl %d", screen_impl);
     if (n == 0 || screen_impl == 2) return SOMB_OK;
     cudaStream_t st = as_stream(stream);
-    int *cand = (int *)ws;
-    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
+    BmuWs w = bmu_carve(ws, n);
+    int *cand = w.cand, *ccount = w.ccount;
     float *thr0 = nullptr;
     if (prev_bmu) {
-        thr0 = (float *)((char *)ccount + align_up((size_t)n * sizeof(int), 256));
+        thr0 = w.thr0;
         const bool three = Xl != nullptr && Wl != nullptr && screen_impl == 0;
         screen_seed_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(
             (const __half *)Xh, three ? (const __half *)Xl : nullptr, n, dp, (const __half *)Wh,
@@ -358,7 +446,7 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
     if (screen_impl == 0)
         return launch_screen_tc((const __half *)Xh, (const __half *)Xl, n, dp, (const __half *)Wh,
                                 (const __half *)Wl, kp, c, xnorm, scal, window_coef, thr0, cand, ccount, flags,
-                                nullptr, (char *)ws + bmu_ws_fixed(n), st);
+                                nullptr, w.ctrs, w.pool, w.ovf_head, w.ovf_lim, st);
     unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
     screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh, kp, c,
                                                       xnorm, scal, window_coef, thr0, cand, ccount, flags);
@@ -376,24 +464,26 @@ extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int3
                  "bmu_rerank: bad dist_mode %d", dist_mode);
     if (n == 0) return SOMB_OK;
     cudaStream_t st = as_stream(stream);
-    int *cand = (int *)ws;
-    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
+    BmuWs bw = bmu_carve(ws, n);
+    int *cand = bw.cand, *ccount = bw.ccount;
     int all = screen_impl == 2, split = screen_impl == 0;
+    OvfView ov{nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (split) ov = OvfView{bw.ovf_head, bw.ovf_lim, bw.pool.ent, bw.pool.next, bw.pool.cnt};
     if (all) cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
     const int wpb = 8;
     const unsigned blocks = (unsigned)((n + wpb - 1) / wpb);
     if (!all && d % 4 == 0 && d <= 1024) {
         if (d <= 128)
-            launch_rerank_vec<1>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, bmu, d2min);
+            launch_rerank_vec<1>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);
         else if (d <= 256)
-            launch_rerank_vec<2>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, bmu, d2min);
+            launch_rerank_vec<2>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);
         else if (d <= 512)
-            launch_rerank_vec<4>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, bmu, d2min);
+            launch_rerank_vec<4>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);
         else
-            launch_rerank_vec<8>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, bmu, d2min);
+            launch_rerank_vec<8>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);
     } else {
         rerank_kernel<<<blocks, 32 * wpb, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, dist_mode, all, split,
-                                                   row_order, bmu, d2min);
+                                                   row_order, ov, bmu, d2min);
     }
     note_launch();
     SOMB_LAUNCH_CHECK("rerank");
@@ -437,10 +527,9 @@ extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, co
                                       int32_t dp, const uint16_t *Wh, const uint16_t *Wl, const float *c, int32_t kp,
                                       const float *scal, float window_coef, float *dump, void *ws, void *stream) {
     int64_t m = n < 128 ? n : 128;
-    int *cand = (int *)ws;
-    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
-    int *flags = (int *)((char *)ccount + align_up((size_t)n * sizeof(int), 256));
+    BmuWs w = bmu_carve(ws, n);
+    int *flags = (int *)w.thr0;
     return launch_screen_tc((const __half *)Xh, (const __half *)Xl, m, dp, (const __half *)Wh, (const __half *)Wl, kp,
-                            c, xnorm, scal, window_coef, nullptr, cand, ccount, flags, dump,
-                            (char *)ws + bmu_ws_fixed(n), as_stream(stream));
+                            c, xnorm, scal, window_coef, nullptr, w.cand, w.ccount, flags, dump, w.ctrs, w.pool,
+                            w.ovf_head, w.ovf_lim, as_stream(stream));
 }

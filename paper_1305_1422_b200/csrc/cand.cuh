@@ -3,7 +3,9 @@
 // A thread owns one data row and visits nodes j in ascending order with
 // screened values r_j.  It keeps every j with r_j <= rmin + win (rmin =
 // running minimum, win = the row's screening window).  If more than CAP
-// nodes fall inside the window, the set is cut to the 3 CAP/4 smallest
+// nodes fall inside the window, the full buffer is spilled to a global
+// overflow pool (when one is given and has room), so the set stays complete.
+// Otherwise the set is cut to the 3 CAP/4 smallest
 // (r, j) pairs in lexicographic order and a cap (capv) is installed: later
 // nodes are accepted only with r < capv (their j is larger than every held
 // index, so (r, j) < (capv, capi) <=> r < capv).  The final set is thus
@@ -55,11 +57,27 @@ __device__ __forceinline__ void cb_st(const CandBuf &b, int e, float v, int j) {
     sts_s32(b.i + e * b.stride, j);
 }
 
+// Overflow pool (optional): when a buffer is full of in-window entries it is
+// spilled as one chunk (<= 32 entries) into a global pool and the row keeps
+// collecting, so the candidate set stays complete; each (row, group) keeps a
+// linked list of its chunks.  Only when the pool is exhausted does the set
+// fall back to truncation.  The re-rank filters spilled entries with the
+// group's final window limit.
+constexpr int kOvfChunk = 32;
+struct OvfPool {
+    int2 *ent;          // [nchunks][kOvfChunk] (value bits, node)
+    int *next;          // [nchunks] next chunk of the same list, -1 = end
+    int *cnt;           // [nchunks] entries used
+    unsigned *ctr;      // chunks allocated so far
+    unsigned nchunks;   // 0 = no pool (truncate when full)
+};
+
 template <int CAP>
 struct CandRow {
     float rmin, thr, capbelow, win;
     int cnt;
-    int trunc;
+    int trunc;          // bit 0: truncated (pool exhausted), bit 1: spilled
+    int head;           // overflow chunk list, -1 = none
 };
 
 template <int CAP>
@@ -72,6 +90,7 @@ __device__ __forceinline__ void cand_init(CandRow<CAP> &s, float win) {
     s.win = win;
     s.cnt = 0;
     s.trunc = 0;
+    s.head = -1;
 }
 
 template <int CAP>
@@ -80,7 +99,7 @@ __device__ __forceinline__ void cand_bound(CandRow<CAP> &s, float r_seen) {
 }
 
 template <int CAP, class Buf>
-__device__ __noinline__ void cand_make_room(CandRow<CAP> &s, Buf b) {
+__device__ __noinline__ void cand_make_room(CandRow<CAP> &s, Buf b, OvfPool pool) {
     const float lim = s.rmin + s.win;
     int m = 0;
     for (int e = 0; e < s.cnt; ++e) {
@@ -93,7 +112,21 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, Buf b) {
     }
     s.cnt = m;
     if (m < CAP) return;
-    // Full inside the window: keep the 3 CAP / 4 smallest (value, index) pairs.
+    // Full inside the window: spill the buffer into the overflow pool ...
+    if (CAP <= kOvfChunk && pool.nchunks) {   // (buffers larger than a chunk never spill)
+        const unsigned c = atomicAdd(pool.ctr, 1u);
+        if (c < pool.nchunks) {
+            int2 *dst = pool.ent + (size_t)c * kOvfChunk;
+            for (int e = 0; e < (CAP < kOvfChunk ? CAP : kOvfChunk); ++e) dst[e] = make_int2(__float_as_int(cb_ldv(b, e)), cb_ldi(b, e));
+            pool.cnt[c] = CAP;
+            pool.next[c] = s.head;
+            s.head = (int)c;
+            s.cnt = 0;
+            s.trunc |= 2;
+            return;
+        }
+    }
+    // ... or, without room there, keep the 3 CAP / 4 smallest (value, index) pairs.
     static_assert(CAP <= 64, "keep mask is 64 bits");
     constexpr int H = 3 * CAP / 4;
     float capv = -INFINITY;
@@ -120,19 +153,20 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, Buf b) {
         }
     }
     s.cnt = m;
-    s.trunc = 1;
+    s.trunc |= 1;
     s.capbelow = fminf(s.capbelow, nextafterf(capv, -INFINITY));
     s.thr = fminf(s.thr, s.capbelow);
 }
 
 template <int CAP, class Buf>
-__device__ __forceinline__ void cand_push(CandRow<CAP> &s, float r, int j, const Buf &b) {
+__device__ __forceinline__ void cand_push(CandRow<CAP> &s, float r, int j, const Buf &b,
+                                          const OvfPool &pool = OvfPool{nullptr, nullptr, nullptr, nullptr, 0u}) {
     if (r <= s.thr) {
         if (r < s.rmin) {
             s.rmin = r;
             s.thr = fminf(s.thr, r + s.win);
         }
-        if (s.cnt == CAP) cand_make_room<CAP>(s, b);
+        if (s.cnt == CAP) cand_make_room<CAP>(s, b, pool);
         if (r <= s.thr) {
             cb_st(b, s.cnt, r, j);
             ++s.cnt;

@@ -228,7 +228,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                                                float wcoef, const float *__restrict__ thr0, int *__restrict__ cand,
                                                int *__restrict__ ccount, int *__restrict__ flags,
                                                float *__restrict__ dump, unsigned *__restrict__ sync_ctr,
-                                               int lag) {
+                                               int lag, OvfPool pool, int *__restrict__ ovf_head,
+                                               float *__restrict__ ovf_lim) {
     using Cfg = TcCfg<CG, PASSES, HC>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -430,7 +431,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                             if (gmin[g8] <= st.thr) {
 #pragma unroll
                                 for (int q = 8 * g8; q < 8 * g8 + 8; ++q)
-                                    if (v[q] <= st.thr) cand_push<Cfg::HALF_CAP>(st, v[q], jc + q, cb);
+                                    if (v[q] <= st.thr) cand_push<Cfg::HALF_CAP>(st, v[q], jc + q, cb, pool);
                             }
                         }
                     }
@@ -449,6 +450,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                 // two column groups write disjoint bytes of ccount / flags
                 reinterpret_cast<uint8_t *>(ccount + row)[half] = (uint8_t)cnt;
                 reinterpret_cast<uint8_t *>(flags + row)[half] = (uint8_t)st.trunc;
+                ovf_head[2 * row + half] = st.head;
+                ovf_lim[2 * row + half] = st.rmin + st.win;
             }
         }
     }
@@ -469,18 +472,19 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
         const __grid_constant__ CUtensorMap map_xl, const __grid_constant__ CUtensorMap map_wl, int64_t n, int dp, int kp, \
         const float *__restrict__ c, const float *__restrict__ xnorm, const float *__restrict__ scal, float wcoef,  \
         const float *__restrict__ thr0, int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags,  \
-        float *__restrict__ dump, unsigned *__restrict__ sync_ctr, int lag
+        float *__restrict__ dump, unsigned *__restrict__ sync_ctr, int lag, OvfPool pool, int *__restrict__ ovf_head, \
+        float *__restrict__ ovf_lim
 
 template <int P, int HC>
 __global__ void __launch_bounds__(TC_THREADS, 1) screen_tc1_kernel(SCREEN_TC_ARGS) {
     screen_tc_body<1, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
-                             flags, dump, sync_ctr, lag);
+                             flags, dump, sync_ctr, lag, pool, ovf_head, ovf_lim);
 }
 
 template <int P, int HC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) screen_tc2_kernel(SCREEN_TC_ARGS) {
     screen_tc_body<2, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
-                             flags, dump, sync_ctr, lag);
+                             flags, dump, sync_ctr, lag, pool, ovf_head, ovf_lim);
 }
 
 // --------------------------------------------------------------- host side
@@ -524,11 +528,10 @@ static int set_smem(KernelT k, uint32_t bytes, const char *what) {
     return r == cudaSuccess ? SOMB_OK : cuda_status(r, what);
 }
 
-size_t screen_tc_scratch_bytes() { return 256; }   // the lockstep counter
-
 int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh, const __half *Wl, int kp,
                      const float *c, const float *xnorm, const float *scal, float wcoef, const float *thr0, int *cand,
-                     int *ccount, int *flags, float *dump, void *scratch, cudaStream_t st) {
+                     int *ccount, int *flags, float *dump, unsigned *ctrs, OvfPool pool, int *ovf_head,
+                     float *ovf_lim, cudaStream_t st) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % TC_BN == 0, SOMB_E_INPUT, "screen_tc: dp %% 8 and kp %% 256 required");
     static bool init = false;
     if (!init) {
@@ -568,15 +571,16 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaMemsetAsync(ccount, 0, (size_t)n * sizeof(int), st);
     cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
-    unsigned *ctr = (unsigned *)scratch;
+    unsigned *ctr = ctrs;              // [0] lockstep, [1] overflow chunks (pool.ctr)
     const int lag = g_lag;
-    if (lag > 0) cudaMemsetAsync(ctr, 0, sizeof(unsigned), st);
+    cudaMemsetAsync(ctrs, 0, 2 * sizeof(unsigned), st);
     const int units = (int)((n + TC_ROWS * cg - 1) / (TC_ROWS * cg));
     const int max_units = sms / cg;
     const int grid = cg * (units < max_units ? units : max_units);
 #define SCREEN_LAUNCH(KERN, CGV, PV, HV)                                                                            \
     KERN<PV, HV><<<grid, TC_THREADS, TcCfg<CGV, PV, HV>::SMEM, st>>>(mx, mw, mxl, mwl, n, dp, kp, c, xnorm, scal, wcoef, \
-                                                                     thr0, cand, ccount, flags, dump, ctr, lag)
+                                                                     thr0, cand, ccount, flags, dump, ctr, lag, pool, \
+                                                                     ovf_head, ovf_lim)
     if (cg == 1) {
         if (three) SCREEN_LAUNCH(screen_tc1_kernel, 1, 3, 16); else SCREEN_LAUNCH(screen_tc1_kernel, 1, 1, 16);
     } else if (three) {

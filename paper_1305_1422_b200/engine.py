@@ -261,6 +261,12 @@ class SomEngine:
             return (cc & 255) + ((cc >> 8) & 255)
         return cc
 
+    def overflow_chunks(self) -> int:
+        """Overflow chunks the last tcgen05 screen spilled (bmu.cu workspace counters)."""
+        a = lambda b: (b + 255) // 256 * 256
+        off = a(self.n * _lib.CAND_CAP * 4) + 2 * a(self.n * 4)
+        return int(self.ws[off + 4: off + 8].view(torch.int32).item())
+
     def qe_sum(self):
         _lib.call("somb_qe_sum", _ptr(self.d2min), self.n, _ptr(self.qe), _ptr(self.ws),
                   _stream(self.dev))

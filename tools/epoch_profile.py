@@ -34,7 +34,9 @@ for e in range(10):
     torch.cuda.synchronize()
     cc = eng.candidate_counts()[: eng.n].float().cpu().numpy()
     fl = eng.flags[: eng.n].cpu().numpy()
-    trunc = float(((fl & 0xFF) | ((fl >> 8) & 0xFF)).astype(bool).mean())
+    trunc = float((((fl & 0xFF) | ((fl >> 8) & 0xFF)) & 1).astype(bool).mean())
+    spilled = float((((fl & 0xFF) | ((fl >> 8) & 0xFF)) & 2).astype(bool).mean())
+    chunks = eng.overflow_chunks() if eng.screen_impl == 0 and eng.passes >= 1 else 0
     eng._mark("node_sums", True)
     eng.qe_sum()
     eng.node_sums()
@@ -46,7 +48,8 @@ for e in range(10):
     ph = {k: round(v[0][0].elapsed_time(v[0][1]), 2) for k, v in eng.timing.items()}
     row = {"epoch": e, "radius": round(r, 2), "scale": round(sc, 3), **ph,
            "cand_mean": round(float(cc.mean()), 2), "cand_p50": float(np.median(cc)),
-           "cand_p99": float(np.percentile(cc, 99)), "cand_max": float(cc.max()), "trunc": trunc}
+           "cand_p99": float(np.percentile(cc, 99)), "cand_max": float(cc.max()), "trunc": trunc,
+           "spilled": spilled, "ovf_chunks": chunks}
     rows.append(row)
     print(json.dumps(row), flush=True)
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
