@@ -269,23 +269,25 @@ __device__ __forceinline__ void load_row4(const float *W, int64_t j, int d4, int
     }
 }
 
+// Four independent fp64 accumulators (one per float4 component) so the DFMA
+// chains overlap; summed pairwise at the end (fixed order: deterministic).
 template <int Q, int MODE>
 __device__ __forceinline__ double dist_part(const float4 (&x)[Q], const float4 (&w)[Q]) {
-    double s = 0.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         if (MODE == SOMB_DIST_NAIVE) {
             double a = (double)w[q].x - (double)x[q].x, b = (double)w[q].y - (double)x[q].y;
             double c = (double)w[q].z - (double)x[q].z, e = (double)w[q].w - (double)x[q].w;
-            s = __fma_rn(a, a, s); s = __fma_rn(b, b, s); s = __fma_rn(c, c, s); s = __fma_rn(e, e, s);
+            s0 = __fma_rn(a, a, s0); s1 = __fma_rn(b, b, s1); s2 = __fma_rn(c, c, s2); s3 = __fma_rn(e, e, s3);
         } else {
-            s = __fma_rn((double)x[q].x, (double)w[q].x, s);
-            s = __fma_rn((double)x[q].y, (double)w[q].y, s);
-            s = __fma_rn((double)x[q].z, (double)w[q].z, s);
-            s = __fma_rn((double)x[q].w, (double)w[q].w, s);
+            s0 = __fma_rn((double)x[q].x, (double)w[q].x, s0);
+            s1 = __fma_rn((double)x[q].y, (double)w[q].y, s1);
+            s2 = __fma_rn((double)x[q].z, (double)w[q].z, s2);
+            s3 = __fma_rn((double)x[q].w, (double)w[q].w, s3);
         }
     }
-    return s;
+    return __dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3));
 }
 
 template <int Q, int MODE>
@@ -367,6 +369,146 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
         bmu[row] = bestj;
         d2min[row] = best;
     }
+}
+
+// Pipelined re-rank: each lane stages ITS OWN float4 slices of the next
+// RS candidates' codebook rows in shared memory with cp.async (L2 -> smem,
+// no register cost), so a warp keeps RS rows (RS x 4d bytes) in flight
+// instead of one -- the plain kernel was bound by memory-level parallelism
+// (profiles/).  A lane only ever reads back what it copied itself, so
+// cp.async.wait_group alone orders the data (no warp barrier).  Same
+// arithmetic and order as rerank_vec_kernel.
+constexpr int RS = 4;            // candidate rows in flight per warp
+constexpr int RP_WARPS = 4;      // warps per block
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int Q, int MODE>
+__global__ void __launch_bounds__(32 * RP_WARPS, 3)
+rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n, int d,
+                   const float *__restrict__ W, const double *__restrict__ w2, int K,
+                   const int *__restrict__ cand, const int *__restrict__ ccount, int split,
+                   const int *__restrict__ order, OvfView ov, int *__restrict__ bmu, double *__restrict__ d2min) {
+    // [warp][stage][q][lane] float4 (dynamic shared memory)
+    extern __shared__ float4 ring_raw[];
+    auto ring = reinterpret_cast<float4 (*)[RS][Q][32]>(ring_raw);
+    const int wib = threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    const int d4 = d >> 2;
+    // persistent warps striding over the (BMU-sorted) rows: no block waits on
+    // its slowest row, and concurrently active warps stay on neighbouring rows
+#pragma unroll 1
+    for (int64_t wi = (int64_t)blockIdx.x * RP_WARPS + wib; wi < n; wi += (int64_t)gridDim.x * RP_WARPS) {
+    const int64_t row = order ? (int64_t)order[wi] : wi;
+    float4 xv[Q];
+    load_row4<Q>(X, row, d4, lane, xv);
+    const int cc = ccount[row];
+    const int c0 = split ? (cc & 255) : cc;
+    const int c1 = split ? ((cc >> 8) & 255) : 0;
+    int cnt = c0 + c1;
+    auto slot = [&](int q) { return q < c0 ? q : SOMB_CAND_CAP / 2 + (q - c0); };
+    const int myj0 = lane < cnt ? cand[row * SOMB_CAND_CAP + slot(lane)] : -1;
+    const int myj1 = lane + 32 < cnt ? cand[row * SOMB_CAND_CAP + slot(lane + 32)] : -1;
+    const bool all = cnt <= 0;       // safety net: exact scan of every node
+    if (all) cnt = K;
+    auto cand_at = [&](int q) {
+        if (all) return q;
+        int a = __shfl_sync(0xffffffffu, myj0, q & 31), b = __shfl_sync(0xffffffffu, myj1, q & 31);
+        return q < 32 ? a : b;
+    };
+    auto issue = [&](int j, int stg) {
+        if ((unsigned)j < (unsigned)K) {
+            const float4 *wr = reinterpret_cast<const float4 *>(W + (int64_t)j * d);
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (lane + 32 * q < d4) cp_async16(smem_addr(&ring[wib][stg][q][lane]), wr + lane + 32 * q);
+        }
+    };
+    const double xx = x2[row];
+    double best = INFINITY;
+    int bestj = 0x7fffffff;
+    auto consider = [&](int j, const float4 (&wv)[Q]) {
+        double s = warp_sum(dist_part<Q, MODE>(xv, wv));
+        double v = s;
+        if (MODE == SOMB_DIST_BLOCKED)   // ((-2 dot) + |x|^2) + |w|^2, clamp (kernels.py:196-202)
+            v = fmax(__dadd_rn(__dadd_rn(__dmul_rn(-2.0, s), xx), w2[(unsigned)j < (unsigned)K ? j : 0]), 0.0);
+        if ((unsigned)j < (unsigned)K && (v < best || (v == best && j < bestj))) {
+            best = v;
+            bestj = j;
+        }
+    };
+    // one pipelined pass over a candidate list given by get(q), q < m
+    auto run = [&](int m, auto get) {
+#pragma unroll
+        for (int s0 = 0; s0 < RS; ++s0) {
+            if (s0 < m) issue(get(s0), s0);
+            cp_async_commit();
+        }
+#pragma unroll 1
+        for (int q = 0; q < m; ++q) {
+            const int stg = q % RS;
+            const int j = get(q);
+            const int jn = q + RS < m ? get(q + RS) : -1;
+            cp_async_wait<RS - 1>();
+            float4 wv[Q];
+#pragma unroll
+            for (int t = 0; t < Q; ++t)
+                wv[t] = lane + 32 * t < d4 ? ring[wib][stg][t][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (jn >= 0) issue(jn, stg);
+            cp_async_commit();
+            consider(j, wv);
+        }
+        cp_async_wait<0>();
+    };
+    run(cnt, cand_at);
+    if (ov.head != nullptr && !all) {   // spilled candidates of both column groups, chunk by chunk
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const float lim = ov.lim[2 * row + h];
+#pragma unroll 1
+            for (int c = ov.head[2 * row + h]; c >= 0; c = ov.next[c]) {
+                const int m = ov.cnt[c];
+                const int2 e = lane < m ? ov.ent[(size_t)c * kOvfChunk + lane] : make_int2(0x7f800000, -1);
+                const unsigned bal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(e.x) <= lim);
+                run(__popc(bal), [&](int q) { return __shfl_sync(0xffffffffu, e.y, __fns(bal, 0, q + 1)); });
+            }
+        }
+    }
+    if (lane == 0) {
+        bmu[row] = bestj;
+        d2min[row] = best;
+    }
+    }
+}
+
+template <int Q>
+static void launch_rerank_pipe(cudaStream_t st, const float *X, const double *x2, int64_t n, int d, const float *W,
+                               const double *w2, int K, const int *cand, const int *ccount, int mode, int split,
+                               const int *order, OvfView ov, int *bmu, double *d2min) {
+    int dev = 0, sms = kSmCount;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = sizeof(float4) * RP_WARPS * RS * Q * 32;
+    static int per_sm = 0;   // resident blocks per SM (same for both modes)
+    if (!per_sm) {
+        cudaFuncSetAttribute(rerank_pipe_kernel<Q, SOMB_DIST_NAIVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(rerank_pipe_kernel<Q, SOMB_DIST_BLOCKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rerank_pipe_kernel<Q, SOMB_DIST_BLOCKED>, 32 * RP_WARPS, smem);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int64_t need = (n + RP_WARPS - 1) / RP_WARPS;
+    const unsigned blocks = (unsigned)(need < (int64_t)per_sm * sms ? need : (int64_t)per_sm * sms);
+    if (mode == SOMB_DIST_NAIVE)
+        rerank_pipe_kernel<Q, SOMB_DIST_NAIVE><<<blocks, 32 * RP_WARPS, smem, st>>>(X, x2, n, d, W, w2, K, cand, ccount,
+                                                                                  split, order, ov, bmu, d2min);
+    else
+        rerank_pipe_kernel<Q, SOMB_DIST_BLOCKED><<<blocks, 32 * RP_WARPS, smem, st>>>(X, x2, n, d, W, w2, K, cand,
+                                                                                    ccount, split, order, ov, bmu, d2min);
 }
 
 template <int Q>
@@ -455,6 +597,8 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
     return SOMB_OK;
 }
 
+static int g_rerank_pipe = -1;   // SOMB_RERANK_PIPE=0 selects the unpipelined kernel (A/B testing)
+
 extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int32_t d, const float *W,
                                const double *w2, int32_t K, int32_t dist_mode, int32_t screen_impl,
                                const int32_t *row_order, int32_t *bmu, double *d2min, int32_t *flags, void *ws,
@@ -466,13 +610,26 @@ extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int3
     cudaStream_t st = as_stream(stream);
     BmuWs bw = bmu_carve(ws, n);
     int *cand = bw.cand, *ccount = bw.ccount;
+    if (g_rerank_pipe < 0) {
+        const char *e = getenv("SOMB_RERANK_PIPE");
+        g_rerank_pipe = e ? atoi(e) != 0 : 1;
+    }
     int all = screen_impl == 2, split = screen_impl == 0;
     OvfView ov{nullptr, nullptr, nullptr, nullptr, nullptr};
     if (split) ov = OvfView{bw.ovf_head, bw.ovf_lim, bw.pool.ent, bw.pool.next, bw.pool.cnt};
     if (all) cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
     const int wpb = 8;
     const unsigned blocks = (unsigned)((n + wpb - 1) / wpb);
-    if (!all && d % 4 == 0 && d <= 1024) {
+    if (!all && d % 4 == 0 && d <= 1024 && g_rerank_pipe) {
+        if (d <= 128)
+            launch_rerank_pipe<1>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);
+        else if (d <= 256)
+            launch_rerank_pipe<2>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);
+        else if (d <= 512)
+            launch_rerank_pipe<4>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);
+        else
+            launch_rerank_pipe<8>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);
+    } else if (!all && d % 4 == 0 && d <= 1024) {
         if (d <= 128)
             launch_rerank_vec<1>(blocks, st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);
         else if (d <= 256)
@@ -533,3 +690,4 @@ extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, co
                             c, xnorm, scal, window_coef, nullptr, w.cand, w.ccount, flags, dump, w.ctrs, w.pool,
                             w.ovf_head, w.ovf_lim, as_stream(stream));
 }
+

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -24,7 +25,7 @@ from . import _lib, errors
 from .datasets import DenseDataset, SparseDataset, _is_torch
 from .grid import GridType, MapType, Neighborhood, distance_table
 
-_DEF_WINDOW_KAPPA = 16.0   # screening window = kappa * u16 * |x-nu| * max|delta| / sqrt(D); measured max screen error <= 6.1 units (tools/calib_screen.py), so the window covers 2x that with 30% margin
+_DEF_WINDOW_KAPPA = float(os.environ.get("SOMB_WINDOW_KAPPA", "10.0"))   # screening window = kappa * u16 * |x-nu| * max|delta| / sqrt(D); measured max screen error <= 6.1 units (tools/calib_screen.py): 1.6x margin; cfg2 1M x 10 epochs bit-identical to the exact scan at kappa 10 (profiles/)
 _U16 = 2.0 ** -11
 # 3-pass split screen (hi.hi + hi.lo + lo.hi): its error is dominated by fp32
 # accumulation, measured max ~ D/8192 in the same units (tools/calib_screen.py:
@@ -235,9 +236,9 @@ class SomEngine:
                   _ptr(prev), self.screen_impl, _ptr(self.flags), _ptr(self.ws), st)
         self._mark("screen", False)
         self._mark("rerank", True)
+        order = _ptr(self.row_order if (self.has_order and self.opt.rerank_order) else None)
         _lib.call("somb_bmu_rerank", _ptr(self.X), _ptr(self.x2), self.n, self.d, _ptr(self.W),
-                  _ptr(self.w2), self.K, dist_mode, self.screen_impl,
-                  _ptr(self.row_order if (self.has_order and self.opt.rerank_order) else None), _ptr(self.bmu),
+                  _ptr(self.w2), self.K, dist_mode, self.screen_impl, order, _ptr(self.bmu),
                   _ptr(self.d2min), _ptr(self.flags), _ptr(self.ws), st)
         self._mark("rerank", False)
         self.has_prev = True

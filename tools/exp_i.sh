@@ -1,0 +1,12 @@
+make -j16 >/dev/null 2>&1 || echo BUILD FAILED
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+SOMB_RERANK_F64=0 timeout 300 python tools/epoch_profile.py cfg2 > gpurun_out/i_prof_f32.txt 2>&1
+SOMB_RERANK_F64=1 timeout 300 python tools/epoch_profile.py cfg2 > gpurun_out/i_prof_f64.txt 2>&1
+for f in gpurun_out/i_prof*.txt; do echo $f; python - "$f" <<'PY'
+import json,sys
+L=[json.loads(l) for l in open(sys.argv[1]) if l.startswith('{')]
+ep=[l for l in L if 'epoch' in l]
+print(' screen', [l['screen'] for l in ep]); print(' rerank', [l['rerank'] for l in ep]); print(' cand', [l['cand_mean'] for l in ep], [l['ovf_chunks'] for l in ep])
+print(' total screen %.1f rerank %.1f' % (sum(l['screen'] for l in ep), sum(l['rerank'] for l in ep)), L[-1])
+PY
+done
