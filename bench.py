@@ -113,8 +113,15 @@ def init_dist(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        # SOMB_DIST_BACKEND=gloo (+ ranks sharing a GPU) exercises the sharded
+        # path on a 1-GPU box; production runs use NCCL, one rank per GPU
+        backend = os.environ.get("SOMB_DIST_BACKEND", "nccl")
+        local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
@@ -228,7 +235,10 @@ def run_ours(args):
     def barrier():
         if world > 1:
             import torch.distributed as dist
-            dist.barrier(device_ids=[local])
+            if dist.get_backend() == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     for s in range(args.warmup):
         r, sc = schedule_for(args.config, s)
@@ -380,7 +390,7 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
-        dist.barrier(device_ids=[local])
+        barrier()
         dist.destroy_process_group()
     return 0
 

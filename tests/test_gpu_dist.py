@@ -1,0 +1,76 @@
+"""Sharded training through the real CUDA kernels on ONE GPU: two ranks
+(gloo process group, both on cuda:0) run train() on partition(n, 2) slices
+with the per-epoch fp64 all-reduce and codebook all-gather of
+engine.SomEngine, and must reproduce the single-process run (the
+reference's distributed equivalence test, test_distributed.py:257-265,
+promises 1e-5; only the fp64 summation order of the all-reduce differs)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _cfg(S, kernel):
+    return S.TrainConfig(n_epochs=5, n_columns=20, n_rows=16, map_type=S.MapType.TOROID, kernel=kernel)
+
+
+def _worker(rank, world, port, x, sparse, out_dir):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1305_1422_b200 as S
+        if sparse:
+            data = S.SparseDataset(*x)
+            kernel = S.Kernel.SPARSE
+        else:
+            data = S.DenseDataset(x)
+            kernel = S.Kernel.DENSE_BLOCKED
+        cb, bmus, u = S.train(data, _cfg(S, kernel), device="cuda:0")
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), w=cb.weights, b=bmus, u=u.heights)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(tmp_path, x, sparse):
+    import torch.multiprocessing as mp
+    import paper_1305_1422_b200 as S
+    mp.spawn(_worker, args=(2, _free_port(), x, sparse, str(tmp_path)), nprocs=2, join=True)
+    data = S.SparseDataset(*x) if sparse else S.DenseDataset(x)
+    kernel = S.Kernel.SPARSE if sparse else S.Kernel.DENSE_BLOCKED
+    cb, bmus, u = S.train(data, _cfg(S, kernel), device="cuda:0")
+    r0, r1 = np.load(tmp_path / "r0.npz"), np.load(tmp_path / "r1.npz")
+    # every rank holds the same replica
+    assert np.array_equal(r0["w"], r1["w"]) and np.array_equal(r0["b"], r1["b"])
+    rel = np.max(np.abs(r0["w"].astype(np.float64) - cb.weights) / np.maximum(np.abs(cb.weights), 1e-12))
+    assert rel <= 1e-5, f"sharded vs single codebook rel err {rel}"
+    assert np.mean(np.any(r0["b"] != bmus, axis=1)) <= 1e-3
+    urel = np.max(np.abs(r0["u"] - u.heights) / np.maximum(np.abs(u.heights), 1e-12))
+    assert urel <= 1e-4
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+def test_sharded_train_dense_two_ranks_one_gpu(tmp_path):
+    rng = np.random.default_rng(5)
+    centers = rng.random((8, 48)).astype(np.float32)
+    x = (centers[rng.integers(0, 8, 6000)] + 0.05 * rng.standard_normal((6000, 48))).astype(np.float32)
+    _run(tmp_path, x, sparse=False)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+def test_sharded_train_sparse_two_ranks_one_gpu(tmp_path):
+    import oracle as O
+    sp = O.gen_random_sparse(3000, 400, 0.02, 11)
+    _run(tmp_path, (sp.n_dimensions, sp.row_offsets, sp.col_indices, sp.values), sparse=True)
