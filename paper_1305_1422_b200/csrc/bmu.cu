@@ -400,6 +400,17 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
     const int wib = threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     const int d4 = d >> 2;
+    // slices this lane owns (bit q: float4 index lane + 32 q < d4); the ring
+    // slots of the others are zeroed once and never written, so reads need
+    // no bounds test (x is zero there too)
+    unsigned vmask = 0u;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (lane + 32 * q < d4) vmask |= 1u << q;
+#pragma unroll
+        for (int s0 = 0; s0 < RS; ++s0)
+            if (lane + 32 * q >= d4) ring[wib][s0][q][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     // persistent warps striding over the (BMU-sorted) rows: no block waits on
     // its slowest row, and concurrently active warps stay on neighbouring rows
 #pragma unroll 1
@@ -426,7 +437,7 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
             const float4 *wr = reinterpret_cast<const float4 *>(W + (int64_t)j * d);
 #pragma unroll
             for (int q = 0; q < Q; ++q)
-                if (lane + 32 * q < d4) cp_async16(smem_addr(&ring[wib][stg][q][lane]), wr + lane + 32 * q);
+                if (vmask >> q & 1u) cp_async16(smem_addr(&ring[wib][stg][q][lane]), wr + lane + 32 * q);
         }
     };
     const double xx = x2[row];
@@ -457,8 +468,7 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
             cp_async_wait<RS - 1>();
             float4 wv[Q];
 #pragma unroll
-            for (int t = 0; t < Q; ++t)
-                wv[t] = lane + 32 * t < d4 ? ring[wib][stg][t][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int t = 0; t < Q; ++t) wv[t] = ring[wib][stg][t][lane];
             if (jn >= 0) issue(jn, stg);
             cp_async_commit();
             consider(j, wv);
