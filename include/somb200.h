@@ -73,6 +73,15 @@ typedef struct somb_hood {
 
 SOMB_API const char *somb_version(void);
 SOMB_API const char *somb_last_error(void);
+/* Tuning / profiling knobs of the tcgen05 screen, settable at run time
+ * (defaults shown; the same names upper-cased with a SOMB_ prefix are read
+ * from the environment once): "screen_lag" 8 (soft lockstep lag in node
+ * tiles, 0 = off), "half_cap" 32 (candidates per row and column group kept
+ * in shared memory before spilling), "tc_group" 2 (CTA-pair MMA; 1 = single
+ * CTA), "tc_multicast" 2 (1-pass screen in 4-CTA clusters whose two pairs
+ * share each codebook tile by TMA multicast; 1 = pairs only), "screen_profile" 0 (1 = skip the epilogue: times the TMA + MMA feed
+ * alone; results are invalid).  Returns SOMB_E_CONFIG for unknown keys. */
+SOMB_API int somb_set_knob(const char *key, int32_t value);
 /* 0 if device `dev` is sm_100 (B200) and the library's kernels load. */
 SOMB_API int somb_device_check(int dev);
 

@@ -58,6 +58,7 @@ SIGNATURES = {
     "somb_bmu_rerank": (C.c_int, [P, P, I64, I32, P, P, I32, I32, I32, P, P, P, P, P, P]),
     "somb_qe_sum": (C.c_int, [P, I64, P, P, P]),
     "somb_launch_count": (C.c_ulonglong, []),
+    "somb_set_knob": (C.c_int, [C.c_char_p, I32]),
     "somb_node_sums_ws": (SZ, [I64, I32, I32]),
     "somb_node_sums_dense": (C.c_int, [P, I64, I32, P, I32, P, P, P, P, P]),
     "somb_hood_ws": (SZ, [C.POINTER(SombMap), I32, I32]),

@@ -37,3 +37,13 @@ extern "C" int somb_device_check(int dev) {
 }
 
 extern "C" unsigned long long somb_launch_count(void) { return somb::g_launches.load(); }
+
+namespace somb {
+int screen_tc_set_knob(const char *key, int value);
+}
+extern "C" int somb_set_knob(const char *key, int32_t value) {
+    SOMB_REQUIRE(key != nullptr, SOMB_E_CONFIG, "set_knob: null key");
+    int rc = somb::screen_tc_set_knob(key, value);
+    if (rc == SOMB_E_CONFIG) somb::set_error("set_knob: unknown key %s", key);
+    return rc;
+}

@@ -47,7 +47,7 @@ constexpr int TC_ROWS = 128;                      // data rows per CTA (TMEM lan
 // near-tied nodes.  A stage holds [A_hi | B_hi | A_lo | B_lo].
 template <int CG, int PASSES = 1, int HC = SOMB_CAND_CAP / 2>
 struct TcCfg {
-    static constexpr int B_ROWS = TC_BN / CG;                      // codebook rows loaded per CTA
+    static constexpr int B_ROWS = TC_BN / CG;                      // codebook rows per CTA (smem B tile)
     static constexpr uint32_t A_BYTES = TC_ROWS * TC_BK * 2;       // 16 KB
     static constexpr uint32_t B_BYTES = B_ROWS * TC_BK * 2;        // 32 KB (CG 1) / 16 KB (CG 2)
     static constexpr uint32_t STAGE_BYTES = (PASSES == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
@@ -133,6 +133,17 @@ __device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const CUtensorMap
     }
 }
 
+// CTA-pair TMA load multicast to the CTAs in `mask` (same smem offset in
+// each); the transaction bytes land on each destination pair's leader barrier.
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
+                                               uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -143,11 +154,11 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 template <int CG>
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
+__device__ __forceinline__ void tc_commit(uint32_t bar, uint16_t mask = 0x3) {
     if constexpr (CG == 1) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
     } else {
-        const uint16_t mask = 0x3;   // both CTAs of the pair, same barrier offset
+        // multicast to the CTAs in `mask` (default: both CTAs of the pair), same barrier offset
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
             "h"(mask)
@@ -220,7 +231,13 @@ __constant__ int g_profile_mode = 0;
 __constant__ int g_a_evict_last = 0;
 
 // ------------------------------------------------------------------ kernel
-template <int CG, int PASSES, int HC>
+// MC = 2 (CG = 2 only): clusters of 4 CTAs = 2 pairs on different rows that
+// sweep the same node tiles; each CTA TMA-loads half of its pair-half of the
+// codebook tile and multicasts it to the same-rank CTA of the other pair, so
+// the L2 -> SM codebook traffic halves (the screen is L2-bandwidth bound).
+// Both pairs' MMAs must release a stage before it is refilled (empty
+// barriers count MC arrivals).
+template <int CG, int PASSES, int HC, int MC = 1>
 __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const CUtensorMap *map_w,
                                                const CUtensorMap *map_xl, const CUtensorMap *map_wl, int64_t n,
                                                int dp, int kp, const float *__restrict__ c,
@@ -242,15 +259,18 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * S + 4);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const uint32_t crank = CG == 2 ? cluster_rank() : 0;
+    const uint32_t cl_rank = CG == 2 ? cluster_rank() : 0;
+    const uint32_t crank = cl_rank & 1u;            // rank within the CTA pair
+    const uint32_t pair = cl_rank >> 1;             // pair within the cluster (MC = 2)
     const bool leader = crank == 0;
+    const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pair));
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t tfull0 = smem_u32(bars + 2 * S), tempty0 = smem_u32(bars + 2 * S + 2);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, MC);   // one MMA-commit arrival per pair sharing the stage
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull0 + 8 * a, 1);
@@ -279,6 +299,10 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
     const int unit_rows = TC_ROWS * CG;
     const int num_units = (int)((n + unit_rows - 1) / unit_rows);
     const int unit0 = blockIdx.x / CG, unit_step = gridDim.x / CG;
+    // iterations: with MC = 2 both pairs of a cluster run the same count (the
+    // later pair may process a zero-filled dummy unit at the tail)
+    const int first_in_cluster = (blockIdx.x / (CG * MC)) * MC;
+    const int iters = first_in_cluster < num_units ? (num_units - first_in_cluster + unit_step - 1) / unit_step : 0;
     const int NT = kp / TC_BN;
     const int KB = (dp + TC_BK - 1) / TC_BK;
 
@@ -294,7 +318,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             const unsigned P = gridDim.x;
             const int waves = (num_units + unit_step - 1) / unit_step;
             unsigned issued = 0;
-            for (int u = unit0; u < num_units; u += unit_step) {
+            for (int it = 0; it < (MC == 1 ? (unit0 < num_units ? (num_units - unit0 + unit_step - 1) / unit_step : 0) : iters); ++it) {
+                const int u = unit0 + it * unit_step;
                 const int row0 = u * unit_rows + TC_ROWS * (int)crank;
                 for (int nt = 0; nt < NT; ++nt) {
                     if (lag > 0 && issued > (unsigned)lag) {
@@ -316,11 +341,25 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                             tma_load_2d_hint<CG>(smem_u32(st0), map_x, fb, kb * TC_BK, row0, pol_a);
                         else
                             tma_load_2d<CG>(smem_u32(st0), map_x, fb, kb * TC_BK, row0);
-                        tma_load_2d<CG>(smem_u32(st0 + Cfg::A_BYTES), map_w, fb, kb * TC_BK, node0);
+                        if constexpr (MC == 1) {
+                            tma_load_2d<CG>(smem_u32(st0 + Cfg::A_BYTES), map_w, fb, kb * TC_BK, node0);
+                        } else {   // my sub-box of the pair-half, multicast to the same rank of both pairs
+                            const uint32_t sub = (uint32_t)pair * (Cfg::B_BYTES / MC);
+                            const uint16_t mcm = (uint16_t)((1u << crank) | (1u << (crank + 2)));
+                            tma_load_2d_mc(smem_u32(st0 + Cfg::A_BYTES + sub), map_w, fb, kb * TC_BK,
+                                           node0 + (Cfg::B_ROWS / MC) * (int)pair, mcm);
+                        }
                         if constexpr (PASSES == 3) {
                             tma_load_2d<CG>(smem_u32(st0 + Cfg::A_BYTES + Cfg::B_BYTES), map_xl, fb, kb * TC_BK, row0);
-                            tma_load_2d<CG>(smem_u32(st0 + 2 * Cfg::A_BYTES + Cfg::B_BYTES), map_wl, fb, kb * TC_BK,
-                                            node0);
+                            if constexpr (MC == 1) {
+                                tma_load_2d<CG>(smem_u32(st0 + 2 * Cfg::A_BYTES + Cfg::B_BYTES), map_wl, fb, kb * TC_BK,
+                                                node0);
+                            } else {
+                                const uint32_t sub = (uint32_t)pair * (Cfg::B_BYTES / MC);
+                                const uint16_t mcm = (uint16_t)((1u << crank) | (1u << (crank + 2)));
+                                tma_load_2d_mc(smem_u32(st0 + 2 * Cfg::A_BYTES + Cfg::B_BYTES + sub), map_wl, fb,
+                                               kb * TC_BK, node0 + (Cfg::B_ROWS / MC) * (int)pair, mcm);
+                            }
                         }
                         if (++stage == S) { stage = 0; phase ^= 1; }
                     }
@@ -340,7 +379,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             uint32_t phase = 0;
             int acc = 0;
             uint32_t aphase = 0;
-            for (int u = unit0; u < num_units; u += unit_step) {
+            const int my_iters = MC == 1 ? (unit0 < num_units ? (num_units - unit0 + unit_step - 1) / unit_step : 0) : iters;
+            for (int it = 0; it < my_iters; ++it) {
                 for (int nt = 0; nt < NT; ++nt) {
                     mbar_wait(tempty0 + 8 * acc, aphase ^ 1);
                     tc_fence_after();
@@ -360,10 +400,10 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                                 tc_mma_f16<CG>(d_tmem, sw128_desc(al + 32 * k), sw128_desc(b0 + 32 * k), Cfg::IDESC, 1);
                             }
                         }
-                        tc_commit<CG>(empty0 + 8 * stage);   // frees the smem slot(s) when these MMAs retire
+                        tc_commit<CG>(empty0 + 8 * stage, MC == 1 ? (uint16_t)0x3 : (uint16_t)0xF);   // frees the smem slot(s) (of both pairs with MC = 2) when these MMAs retire
                         if (++stage == S) { stage = 0; phase ^= 1; }
                     }
-                    tc_commit<CG>(tfull0 + 8 * acc);         // accumulator ready for the epilogue(s)
+                    tc_commit<CG>(tfull0 + 8 * acc, pair_mask);   // accumulator ready for the pair's epilogues
                     if (++acc == 2) { acc = 0; aphase ^= 1; }
                 }
             }
@@ -382,7 +422,9 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
         const CandBuf cb{smem_u32(cbv + et), smem_u32(cbi + et), 4u * TC_EPI_WARPS * 32};
         int acc = 0;
         uint32_t aphase = 0;
-        for (int u = unit0; u < num_units; u += unit_step) {
+        const int my_iters = MC == 1 ? (unit0 < num_units ? (num_units - unit0 + unit_step - 1) / unit_step : 0) : iters;
+        for (int it = 0; it < my_iters; ++it) {
+            const int u = unit0 + it * unit_step;
             const int64_t row = (int64_t)u * unit_rows + TC_ROWS * crank + quad * 32 + lane;
             const bool live = row < n;
             CandRow<Cfg::HALF_CAP> st;
@@ -396,7 +438,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     __syncwarp();
                     if (lane == 0) {
                         if (CG == 1 || leader) mbar_arrive_local(tempty0 + 8 * acc);
-                        else mbar_arrive_cluster(tempty0 + 8 * acc, 0);
+                        else mbar_arrive_cluster(tempty0 + 8 * acc, cl_rank & ~1u);
                     }
                     if (++acc == 2) { acc = 0; aphase ^= 1; }
                     continue;
@@ -440,7 +482,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                 __syncwarp();
                 if (lane == 0) {
                     if (CG == 1 || leader) mbar_arrive_local(tempty0 + 8 * acc);
-                    else mbar_arrive_cluster(tempty0 + 8 * acc, 0);
+                    else mbar_arrive_cluster(tempty0 + 8 * acc, cl_rank & ~1u);
                 }
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
@@ -479,6 +521,12 @@ template <int P, int HC>
 __global__ void __launch_bounds__(TC_THREADS, 1) screen_tc1_kernel(SCREEN_TC_ARGS) {
     screen_tc_body<1, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
                              flags, dump, sync_ctr, lag, pool, ovf_head, ovf_lim);
+}
+
+template <int P, int HC>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1) screen_tc4_kernel(SCREEN_TC_ARGS) {
+    screen_tc_body<2, P, HC, 2>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
+                                flags, dump, sync_ctr, lag, pool, ovf_head, ovf_lim);
 }
 
 template <int P, int HC>
@@ -521,6 +569,7 @@ static int make_map(CUtensorMap *map, const void *base, uint64_t inner, uint64_t
 static int g_tc_group = 2;   // SOMB_TC_GROUP=1 selects the single-CTA variant (A/B testing)
 static int g_half_cap = 32;  // SOMB_HALF_CAP = 8 | 16 | 32: candidates kept per (row, column group)
 static int g_lag = 8;        // SOMB_SCREEN_LAG: soft lockstep of the CTAs' codebook sweeps (0 = off)
+static int g_mc = 2;         // SOMB_TC_MULTICAST: 2 = 4-CTA clusters multicasting the codebook tiles (1-pass screen), 1 = off
 
 template <class KernelT>
 static int set_smem(KernelT k, uint32_t bytes, const char *what) {
@@ -528,43 +577,70 @@ static int set_smem(KernelT k, uint32_t bytes, const char *what) {
     return r == cudaSuccess ? SOMB_OK : cuda_status(r, what);
 }
 
+static int screen_tc_init() {
+    static bool init = false;
+    if (init) return SOMB_OK;
+    const char *e = getenv("SOMB_TC_GROUP");
+    if (e && atoi(e) == 1) g_tc_group = 1;
+    const char *hc = getenv("SOMB_HALF_CAP");
+    if (hc) g_half_cap = atoi(hc) <= 8 ? 8 : atoi(hc) <= 16 ? 16 : 32;
+    const char *lg = getenv("SOMB_SCREEN_LAG");
+    if (lg) g_lag = atoi(lg);
+    const char *mc = getenv("SOMB_TC_MULTICAST");
+    if (mc) g_mc = atoi(mc) == 2 ? 2 : 1;
+    const char *pm = getenv("SOMB_SCREEN_PROFILE");
+    int mode = pm ? atoi(pm) : 0;
+    cudaMemcpyToSymbol(g_profile_mode, &mode, sizeof(int));
+    const char *ae = getenv("SOMB_A_EVICT_LAST");
+    int a_last = ae ? atoi(ae) : 0;
+    cudaMemcpyToSymbol(g_a_evict_last, &a_last, sizeof(int));
+    int rc = set_smem(screen_tc1_kernel<1, 16>, TcCfg<1, 1, 16>::SMEM, "screen_tc1 smem");
+    if (!rc) rc = set_smem(screen_tc1_kernel<3, 16>, TcCfg<1, 3, 16>::SMEM, "screen_tc1x3 smem");
+    if (!rc) rc = set_smem(screen_tc2_kernel<1, 8>, TcCfg<2, 1, 8>::SMEM, "screen_tc2 smem");
+    if (!rc) rc = set_smem(screen_tc2_kernel<1, 16>, TcCfg<2, 1, 16>::SMEM, "screen_tc2 smem");
+    if (!rc) rc = set_smem(screen_tc2_kernel<1, 32>, TcCfg<2, 1, 32>::SMEM, "screen_tc2 smem");
+    if (!rc) rc = set_smem(screen_tc2_kernel<3, 8>, TcCfg<2, 3, 8>::SMEM, "screen_tc2x3 smem");
+    if (!rc) rc = set_smem(screen_tc2_kernel<3, 16>, TcCfg<2, 3, 16>::SMEM, "screen_tc2x3 smem");
+    if (!rc) rc = set_smem(screen_tc2_kernel<3, 32>, TcCfg<2, 3, 32>::SMEM, "screen_tc2x3 smem");
+    if (!rc) rc = set_smem(screen_tc4_kernel<1, 32>, TcCfg<2, 1, 32>::SMEM, "screen_tc4 smem");
+    if (!rc) rc = set_smem(screen_tc4_kernel<3, 32>, TcCfg<2, 3, 32>::SMEM, "screen_tc4x3 smem");
+    if (rc) return rc;
+    init = true;
+    return SOMB_OK;
+}
+
+// runtime tuning knobs (somb_set_knob): "screen_lag", "screen_profile", "half_cap", "tc_group"
+int screen_tc_set_knob(const char *key, int value) {
+    int rc = screen_tc_init();
+    if (rc) return rc;
+    if (!strcmp(key, "screen_lag")) { g_lag = value; return SOMB_OK; }
+    if (!strcmp(key, "half_cap")) { g_half_cap = value <= 8 ? 8 : value <= 16 ? 16 : 32; return SOMB_OK; }
+    if (!strcmp(key, "tc_group")) { g_tc_group = value == 1 ? 1 : 2; return SOMB_OK; }
+    if (!strcmp(key, "tc_multicast")) { g_mc = value == 2 ? 2 : 1; return SOMB_OK; }
+    if (!strcmp(key, "screen_profile")) {
+        cudaError_t r = cudaMemcpyToSymbol(g_profile_mode, &value, sizeof(int));
+        return r == cudaSuccess ? SOMB_OK : cuda_status(r, "set screen_profile");
+    }
+    return SOMB_E_CONFIG;
+}
+
 int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh, const __half *Wl, int kp,
                      const float *c, const float *xnorm, const float *scal, float wcoef, const float *thr0, int *cand,
                      int *ccount, int *flags, float *dump, unsigned *ctrs, OvfPool pool, int *ovf_head,
                      float *ovf_lim, cudaStream_t st) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % TC_BN == 0, SOMB_E_INPUT, "screen_tc: dp %% 8 and kp %% 256 required");
-    static bool init = false;
-    if (!init) {
-        const char *e = getenv("SOMB_TC_GROUP");
-        if (e && atoi(e) == 1) g_tc_group = 1;
-        const char *hc = getenv("SOMB_HALF_CAP");
-        if (hc) g_half_cap = atoi(hc) <= 8 ? 8 : atoi(hc) <= 16 ? 16 : 32;
-        const char *lg = getenv("SOMB_SCREEN_LAG");
-        if (lg) g_lag = atoi(lg);
-        const char *pm = getenv("SOMB_SCREEN_PROFILE");
-        int mode = pm ? atoi(pm) : 0;
-        cudaMemcpyToSymbol(g_profile_mode, &mode, sizeof(int));
-        const char *ae = getenv("SOMB_A_EVICT_LAST");
-        int a_last = ae ? atoi(ae) : 0;
-        cudaMemcpyToSymbol(g_a_evict_last, &a_last, sizeof(int));
-        int rc = set_smem(screen_tc1_kernel<1, 16>, TcCfg<1, 1, 16>::SMEM, "screen_tc1 smem");
-        if (!rc) rc = set_smem(screen_tc1_kernel<3, 16>, TcCfg<1, 3, 16>::SMEM, "screen_tc1x3 smem");
-        if (!rc) rc = set_smem(screen_tc2_kernel<1, 8>, TcCfg<2, 1, 8>::SMEM, "screen_tc2 smem");
-        if (!rc) rc = set_smem(screen_tc2_kernel<1, 16>, TcCfg<2, 1, 16>::SMEM, "screen_tc2 smem");
-        if (!rc) rc = set_smem(screen_tc2_kernel<1, 32>, TcCfg<2, 1, 32>::SMEM, "screen_tc2 smem");
-        if (!rc) rc = set_smem(screen_tc2_kernel<3, 8>, TcCfg<2, 3, 8>::SMEM, "screen_tc2x3 smem");
-        if (!rc) rc = set_smem(screen_tc2_kernel<3, 16>, TcCfg<2, 3, 16>::SMEM, "screen_tc2x3 smem");
-        if (!rc) rc = set_smem(screen_tc2_kernel<3, 32>, TcCfg<2, 3, 32>::SMEM, "screen_tc2x3 smem");
-        if (rc) return rc;
-        init = true;
-    }
+    int rc0 = screen_tc_init();
+    if (rc0) return rc0;
     const int cg = g_tc_group;
+    // multicast variant: CTA pairs, full capacity, 1-pass (the 3-pass screen is
+    // MMA-bound, and 4-CTA cluster packing can leave SMs idle)
     const bool three = Xl != nullptr && Wl != nullptr;
+    const int mcv = cg == 2 && g_half_cap == 32 && !three ? g_mc : 1;
     CUtensorMap mx, mw, mxl, mwl;
     int rc = make_map(&mx, Xh, (uint64_t)dp, (uint64_t)n, TC_ROWS);
-    if (!rc) rc = make_map(&mw, Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg));
+    if (!rc) rc = make_map(&mw, Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg / mcv));
     if (!rc) rc = make_map(&mxl, three ? Xl : Xh, (uint64_t)dp, (uint64_t)n, TC_ROWS);
-    if (!rc) rc = make_map(&mwl, three ? Wl : Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg));
+    if (!rc) rc = make_map(&mwl, three ? Wl : Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg / mcv));
     if (rc) return rc;
     int dev = 0, sms = kSmCount;
     cudaGetDevice(&dev);
@@ -575,14 +651,37 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
     const int lag = g_lag;
     cudaMemsetAsync(ctrs, 0, 2 * sizeof(unsigned), st);
     const int units = (int)((n + TC_ROWS * cg - 1) / (TC_ROWS * cg));
-    const int max_units = sms / cg;
-    const int grid = cg * (units < max_units ? units : max_units);
+    int max_units = sms / cg;
+    if (mcv == 2) {   // co-resident 4-CTA clusters (GPC packing can leave SMs idle)
+        static int max_clusters = 0;
+        if (!max_clusters) {
+            cudaLaunchConfig_t lc = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 4;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.gridDim = dim3(4 * (sms / 4));
+            lc.blockDim = dim3(TC_THREADS);
+            lc.dynamicSmemBytes = TcCfg<2, 1, 32>::SMEM;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&max_clusters, screen_tc4_kernel<1, 32>, &lc) != cudaSuccess ||
+                max_clusters < 1)
+                max_clusters = sms / 4;
+        }
+        max_units = 2 * max_clusters;
+    }
+    int grid = cg * (units < max_units ? units : max_units);
+    if (mcv == 2) grid = 4 * ((grid + 3) / 4);
 #define SCREEN_LAUNCH(KERN, CGV, PV, HV)                                                                            \
     KERN<PV, HV><<<grid, TC_THREADS, TcCfg<CGV, PV, HV>::SMEM, st>>>(mx, mw, mxl, mwl, n, dp, kp, c, xnorm, scal, wcoef, \
                                                                      thr0, cand, ccount, flags, dump, ctr, lag, pool, \
                                                                      ovf_head, ovf_lim)
     if (cg == 1) {
         if (three) SCREEN_LAUNCH(screen_tc1_kernel, 1, 3, 16); else SCREEN_LAUNCH(screen_tc1_kernel, 1, 1, 16);
+    } else if (mcv == 2) {
+        if (three) SCREEN_LAUNCH(screen_tc4_kernel, 2, 3, 32); else SCREEN_LAUNCH(screen_tc4_kernel, 2, 1, 32);
     } else if (three) {
         if (g_half_cap == 8) SCREEN_LAUNCH(screen_tc2_kernel, 2, 3, 8);
         else if (g_half_cap == 16) SCREEN_LAUNCH(screen_tc2_kernel, 2, 3, 16);
