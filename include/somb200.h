@@ -156,6 +156,17 @@ SOMB_API int somb_bmu_rerank(const float *X, const double *x2, int64_t n,
                              const int32_t *row_order, int32_t *bmu, double *d2min,
                              int32_t *flags, void *ws, void *stream);
 
+/* The whole BMU search in one call: somb_bmu_screen (seeded from
+ * prev_bmu, may be NULL) + somb_bmu_rerank (visiting rows in row_order,
+ * may be NULL).  ws >= somb_bmu_ws(n). */
+SOMB_API int somb_bmu_search(const uint16_t *Xh, const uint16_t *Xl, const float *X, const float *xnorm,
+                             const double *x2, int64_t n, int32_t d, int32_t dp, const uint16_t *Wh,
+                             const uint16_t *Wl, const float *W, const float *c, const double *w2,
+                             int32_t K, int32_t kp, const float *scal, float window_coef,
+                             const int32_t *prev_bmu, const int32_t *row_order, int32_t dist_mode,
+                             int32_t screen_impl, int32_t *bmu, double *d2min, int32_t *flags,
+                             void *ws, void *stream);
+
 /* qe_sum = sum_i sqrt(d2min_i) in fixed order (kernels.py:407, 427). */
 SOMB_API int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws,
                 void *stream);

@@ -56,6 +56,8 @@ SIGNATURES = {
     "somb_bmu_screen": (C.c_int, [P, P, P, I64, I32, P, P, P, I32, I32, P, F32, P, I32, P, P, P]),
     "somb_debug_screen_dump": (C.c_int, [P, P, P, I64, I32, P, P, P, I32, P, F32, P, P, P]),
     "somb_bmu_rerank": (C.c_int, [P, P, I64, I32, P, P, I32, I32, I32, P, P, P, P, P, P]),
+    "somb_bmu_search": (C.c_int, [P, P, P, P, P, I64, I32, I32, P, P, P, P, P, I32, I32, P, F32, P, P, I32,
+                                  I32, P, P, P, P, P]),
     "somb_qe_sum": (C.c_int, [P, I64, P, P, P]),
     "somb_launch_count": (C.c_ulonglong, []),
     "somb_set_knob": (C.c_int, [C.c_char_p, I32]),

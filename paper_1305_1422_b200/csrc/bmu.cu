@@ -701,3 +701,18 @@ extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, co
                             w.ovf_head, w.ovf_lim, as_stream(stream));
 }
 
+
+// Full BMU search in one call: previous-BMU seed + screen + exact re-rank.
+extern "C" int somb_bmu_search(const uint16_t *Xh, const uint16_t *Xl, const float *X, const float *xnorm,
+                               const double *x2, int64_t n, int32_t d, int32_t dp, const uint16_t *Wh,
+                               const uint16_t *Wl, const float *W, const float *c, const double *w2, int32_t K,
+                               int32_t kp, const float *scal, float window_coef, const int32_t *prev_bmu,
+                               const int32_t *row_order, int32_t dist_mode, int32_t screen_impl, int32_t *bmu,
+                               double *d2min, int32_t *flags, void *ws, void *stream) {
+    SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && dp % 8 == 0 && kp >= K && kp % 256 == 0, SOMB_E_INPUT,
+                 "bmu_search: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
+    int rc = somb_bmu_screen(Xh, Xl, xnorm, n, dp, Wh, Wl, c, K, kp, scal, window_coef, prev_bmu, screen_impl, flags,
+                             ws, stream);
+    if (rc) return rc;
+    return somb_bmu_rerank(X, x2, n, d, W, w2, K, dist_mode, screen_impl, row_order, bmu, d2min, flags, ws, stream);
+}

@@ -352,3 +352,25 @@ def test_sparse_random_vs_oracle():
     assert qe == pytest.approx(oqe, rel=1e-12)
     np.testing.assert_allclose(acc.numerators, num, rtol=1e-11, atol=1e-12)
     np.testing.assert_allclose(acc.denominators, den, rtol=1e-11, atol=1e-12)
+
+
+def test_bmu_search_one_call_matches_phases():
+    """somb_bmu_search (seed + screen + re-rank in one C call) == the engine's
+    separate somb_bmu_screen / somb_bmu_rerank phases, bit for bit."""
+    import ctypes as C
+    from paper_1305_1422_b200 import _lib
+    from paper_1305_1422_b200.engine import SomEngine, _ptr, _stream
+    rng = np.random.default_rng(3)
+    x = rng.random((5000, 300), dtype=np.float32)
+    eng = SomEngine(x, 30, 20, S.MapType.TOROID, device="cuda:0")
+    eng.set_codebook(rng.random((600, 300), dtype=np.float32))
+    eng.search()
+    ref_b, ref_d = eng.bmu[: eng.n].clone(), eng.d2min[: eng.n].clone()
+    bmu = torch.full_like(eng.bmu, -1)
+    d2 = torch.zeros_like(eng.d2min)
+    _lib.call("somb_bmu_search", _ptr(eng.Xh), _ptr(eng.Xl), _ptr(eng.X), _ptr(eng.xnorm), _ptr(eng.x2), eng.n,
+              eng.d, eng.dp, _ptr(eng.Wh), _ptr(eng.Wl), _ptr(eng.W), _ptr(eng.c), _ptr(eng.w2), eng.K, eng.kp,
+              _ptr(eng.scal), C.c_float(eng.window_coef), _ptr(ref_b), None, _lib.DIST_BLOCKED, 0,
+              _ptr(bmu), _ptr(d2), _ptr(eng.flags), _ptr(eng.ws), _stream(eng.dev))
+    torch.cuda.synchronize()
+    assert torch.equal(bmu[: eng.n], ref_b) and torch.equal(d2[: eng.n], ref_d)
