@@ -204,6 +204,31 @@ __device__ __forceinline__ int spec_key(const SpecGeom &g, int yo, int yi) {
     return dy * 3 + (sh + 1);
 }
 
+// Dense DFT operands, built once per update so the GEMM loaders are plain
+// loads: Phi [2F][nx] (cos rows, then -sin rows; forward, real -> complex)
+// and Psi [nx][2F] (inverse with the real-signal weights w_f / L).
+__global__ void spec_dft_mats(SpecGeom g, const double *__restrict__ cs, const double *__restrict__ sn,
+                              double *__restrict__ phi, double *__restrict__ psi) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t tot = (int64_t)2 * g.F * g.nx;
+    if (e >= tot) return;
+    const int r = (int)(e / g.nx), c = (int)(e % g.nx);
+    const int plane = r >= g.F, f = r - plane * g.F;
+    const int q = (int)(((int64_t)f * c) % g.L);
+    phi[e] = plane ? -sn[q] : cs[q];
+    const double w = (f == 0 || 2 * f == g.L) ? 1.0 : 2.0;
+    psi[(int64_t)c * 2 * g.F + r] = w * (plane ? -sn[q] : cs[q]) / (double)g.L;
+}
+
+// ktT [f][key][2]: the kernel spectra regrouped per frequency (MidA locality)
+__global__ void spec_ktab_T(int nkeys, int F, const double *__restrict__ ktab, double *__restrict__ ktT) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nkeys * F) return;
+    const int key = e / F, f = e % F;
+    ktT[((int64_t)f * nkeys + key) * 2 + 0] = ktab[((int64_t)key * 2 + 0) * F + f];
+    ktT[((int64_t)f * nkeys + key) * 2 + 1] = ktab[((int64_t)key * 2 + 1) * F + f];
+}
+
 // k^[key][f] = sum_t k[t] w^{-f t}; ktab layout [key][2][F] (re, im)
 __global__ void spec_kernel_table(SpecGeom g, const double *__restrict__ htab, const double *__restrict__ cs,
                                   const double *__restrict__ sn, double *__restrict__ ktab) {
@@ -257,12 +282,8 @@ __global__ void spec_kernel_table(SpecGeom g, const double *__restrict__ htab, c
 // ----------------------------------------------------------- GEMM operands
 // fwd: A = Phi [2F x nx] (cos rows then -sin rows), B = S_y [nx x D]
 struct FwdA {
-    SpecGeom g; const double *cs, *sn;
-    __device__ double operator()(int, int r, int c) const {
-        int f = r < g.F ? r : r - g.F;
-        int q = (int)(((int64_t)f * c) % g.L);
-        return r < g.F ? cs[q] : -sn[q];
-    }
+    const double *phi; int nx;
+    __device__ double operator()(int, int r, int c) const { return phi[(int64_t)r * nx + c]; }
 };
 // column d == D carries the BMU counts, so den = H cnt rides the same DFTs
 struct FwdB {
@@ -282,13 +303,13 @@ struct FwdEp {
 };
 // mid: per f, [Nr; Ni] = [[Kr, -Ki], [Ki, Kr]] [Sr; Si], rows y_out in [y0, y0+nyo)
 struct MidA {
-    SpecGeom g; const double *ktab; int y0, nyo;
+    SpecGeom g; const double *ktT; int nkeys, y0, nyo;
     __device__ double operator()(int f, int r, int k) const {
         int pr = r >= nyo, pk = k >= g.ny;
         int yo = y0 + r - pr * nyo, yi = k - pk * g.ny;
         int key = spec_key(g, yo, yi);
-        double kr = ktab[((int64_t)key * 2 + 0) * g.F + f];
-        double ki = ktab[((int64_t)key * 2 + 1) * g.F + f];
+        const double2 kk = *reinterpret_cast<const double2 *>(ktT + ((int64_t)f * nkeys + key) * 2);
+        double kr = kk.x, ki = kk.y;
         if (!pr) return pk ? -ki : kr;
         return pk ? kr : ki;
     }
@@ -330,14 +351,8 @@ struct DenEp {
 };
 // inv: num_y [nx x D] = Psi [nx x 2F] * [Nr_y; Ni_y]
 struct InvA {
-    SpecGeom g; const double *cs, *sn;
-    __device__ double operator()(int, int c, int q2) const {
-        int plane = q2 >= g.F, f = q2 - plane * g.F;
-        double w = (f == 0 || 2 * f == g.L) ? 1.0 : 2.0;
-        int q = (int)(((int64_t)f * c) % g.L);
-        double v = plane ? -sn[q] : cs[q];
-        return w * v / (double)g.L;
-    }
+    const double *psi; int F2;
+    __device__ double operator()(int, int c, int q2) const { return psi[(int64_t)c * F2 + q2]; }
 };
 struct InvB {
     SpecGeom g; const double *Nh; int nyo, Dp1;
@@ -386,7 +401,8 @@ static int spec_nkeys(const SpecGeom &g) {
 size_t spec_ws_bytes(const somb_map *m, int d) {
     SpecGeom g = spec_geom(m);
     size_t b = 2 * align_up((size_t)g.L * 8, 256);
-    b += align_up((size_t)spec_nkeys(g) * 2 * g.F * 8, 256);
+    b += 2 * align_up((size_t)spec_nkeys(g) * 2 * g.F * 8, 256);   // ktab + per-frequency copy
+    b += 2 * align_up((size_t)2 * g.F * g.nx * 8, 256);             // Phi, Psi
     b += align_up((size_t)2 * g.F * g.ny * (d + 1) * 8, 256);      // Shat (+ count channel)
     b += align_up((size_t)2 * g.F * g.ny * (d + 1) * 8, 256);      // Nhat (worst case: all rows)
     return b;
@@ -404,6 +420,9 @@ int spec_update(const somb_map *m, const double *htab, const double *S, const do
     double *sn = (double *)take((size_t)g.L * 8);
     const int nkeys = spec_nkeys(g);
     double *ktab = (double *)take((size_t)nkeys * 2 * g.F * 8);
+    double *ktT = (double *)take((size_t)nkeys * 2 * g.F * 8);
+    double *phi = (double *)take((size_t)2 * g.F * g.nx * 8);
+    double *psi = (double *)take((size_t)2 * g.F * g.nx * 8);
     const int Dp1 = d + 1;
     double *Sh = (double *)take((size_t)2 * g.F * g.ny * Dp1 * 8);
     const int y0 = j0 / g.nx, y1 = (j1 + g.nx - 1) / g.nx, nyo = y1 - y0;
@@ -412,12 +431,17 @@ int spec_update(const somb_map *m, const double *htab, const double *S, const do
     note_launch();
     spec_kernel_table<<<nkeys, 256, (size_t)g.L * 8, st>>>(g, htab, cs, sn, ktab);
     note_launch();
+    spec_ktab_T<<<(nkeys * g.F + 255) / 256, 256, 0, st>>>(nkeys, g.F, ktab, ktT);
+    note_launch();
+    spec_dft_mats<<<(unsigned)(((int64_t)2 * g.F * g.nx + 255) / 256), 256, 0, st>>>(g, cs, sn, phi, psi);
+    note_launch();
     const int nc = den_mode ? Dp1 : d;     // channels carried through the DFTs
-    dgemm_launch(g.ny, 2 * g.F, nc, g.nx, FwdA{g, cs, sn}, FwdB{g, S, cnt, d}, FwdEp{g, Sh, Dp1}, st);
-    dgemm_launch(g.F, 2 * nyo, nc, 2 * g.ny, MidA{g, ktab, y0, nyo}, MidB{g, Sh, Dp1}, MidEp{g, Nh, nyo, Dp1}, st);
+    dgemm_launch(g.ny, 2 * g.F, nc, g.nx, FwdA{phi, g.nx}, FwdB{g, S, cnt, d}, FwdEp{g, Sh, Dp1}, st);
+    dgemm_launch(g.F, 2 * nyo, nc, 2 * g.ny, MidA{g, ktT, nkeys, y0, nyo}, MidB{g, Sh, Dp1}, MidEp{g, Nh, nyo, Dp1},
+                 st);
     if (den_mode)
-        dgemm_launch(nyo, g.nx, 1, 2 * g.F, InvA{g, cs, sn}, DenB{g, Nh, nyo, Dp1}, DenEp{g, y0, j0, j1, tau, den}, st);
-    dgemm_launch(nyo, g.nx, d, 2 * g.F, InvA{g, cs, sn}, InvB{g, Nh, nyo, Dp1},
+        dgemm_launch(nyo, g.nx, 1, 2 * g.F, InvA{psi, 2 * g.F}, DenB{g, Nh, nyo, Dp1}, DenEp{g, y0, j0, j1, tau, den}, st);
+    dgemm_launch(nyo, g.nx, d, 2 * g.F, InvA{psi, 2 * g.F}, InvB{g, Nh, nyo, Dp1},
                  InvEp{g, y0, j0, j1, d, den, scale, 1.0 - scale, Wold, Wnew, num_out}, st);
     SOMB_LAUNCH_CHECK("spectral hood update");
     return SOMB_OK;
