@@ -222,7 +222,9 @@ SOMB_API int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const fl
                              const float *scal, const double *x2, const float *xnorm,
                              float window_coef, int32_t exact, int32_t *bmu,
                              double *d2min, int32_t *flags, void *ws, void *stream);
-/* S (K x d, fp64, dense) / cnt from CSR rows; ws >= somb_node_sums_ws(n, 1, K). */
+/* S (K x d, fp64, dense) / cnt from CSR rows; ws >= somb_node_sums_ws(n, d, K).
+ * Nodes with more than 2048 rows are summed in 2048-row segments folded in
+ * segment order (the dense path's scheme), else in ascending row order. */
 SOMB_API int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col,
                                    const float *val, int64_t n, int32_t d,
                                    const int32_t *bmu, int32_t K, double *S,

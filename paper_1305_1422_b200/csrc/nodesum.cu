@@ -131,14 +131,14 @@ __global__ void bucket_count(const int *__restrict__ bmu, int64_t n, int *__rest
 }
 
 __global__ void seg_plan(const int *__restrict__ cnt, int K, int *__restrict__ nseg,
-                         int *__restrict__ mseg, double *__restrict__ cnt_out) {
+                         int *__restrict__ mseg, double *__restrict__ cnt_out, int seg = kSeg) {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= K) return;
     int c = cnt[b];
-    int s = (c + kSeg - 1) / kSeg;
+    int s = (c + seg - 1) / seg;
     nseg[b] = s;
     mseg[b] = s > 1 ? s : 0;
-    cnt_out[b] = (double)c;
+    if (cnt_out) cnt_out[b] = (double)c;
 }
 
 // One block per 256-row segment of one node: fixed-order fp64 sum.
@@ -309,6 +309,26 @@ extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const 
 }
 
 namespace somb {
+// Segment plan of the sorted rows for per-node sums in fixed-size row
+// segments (the sparse path; the dense path plans inside
+// somb_node_sums_dense): nseg/segoff per node, msegoff = partial-slot
+// offsets of multi-segment nodes.  ws is carved like somb_node_sums_ws.
+void node_seg_plan(void *ws, int64_t n, int d, int K, int seg, int **nseg, int **segoff, int **msegoff,
+                   double **P, size_t *P_doubles, cudaStream_t st) {
+    NodeSumWs w = carve(ws, n, d, K);
+    seg_plan<<<(K + 255) / 256, 256, 0, st>>>(w.cnt, K, w.nseg, w.mseg, nullptr, seg);
+    note_launch();
+    exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.nseg, K, w.segoff);
+    note_launch();
+    exclusive_scan_kernel<<<1, 1024, 0, st>>>(w.mseg, K, w.msegoff);
+    note_launch();
+    *nseg = w.nseg;
+    *segoff = w.segoff;
+    *msegoff = w.msegoff;
+    *P = w.P;
+    *P_doubles = ((size_t)2 * ((n + kSeg - 1) / kSeg) + 2) * d;
+}
+
 int exclusive_scan(const int *in, int len, int *out, cudaStream_t st) {
     exclusive_scan_kernel<<<1, 1024, 0, st>>>(in, len, out);
     note_launch();

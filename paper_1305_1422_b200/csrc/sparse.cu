@@ -153,24 +153,53 @@ __global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *
     }
 }
 
-// S_b = sum of the rows of node b in ascending row order (sparse scatter into
-// the dense fp64 K x d accumulator; a row's columns are unique, so the threads
-// of a block never collide); kernels.py:229-242 regrouped by BMU.
-__global__ void sp_node_sums_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col,
-                                    const float *__restrict__ val, int d, const int *__restrict__ perm,
-                                    const int *__restrict__ off, int K, double *__restrict__ S) {
-    const int b = blockIdx.x;
-    if (b >= K) return;
-    double *sb = S + (int64_t)b * d;
-    for (int t = off[b]; t < off[b + 1]; ++t) {
+int node_bucket_sort(const int *bmu, int64_t n, int K, void *ws, const int **perm, const int **off, double *cnt,
+                     cudaStream_t st);
+void node_seg_plan(void *ws, int64_t n, int d, int K, int seg, int **nseg, int **segoff, int **msegoff, double **P,
+                   size_t *P_doubles, cudaStream_t st);
+
+// Large nodes (the reference's degenerate sparse fixed point maps every row
+// to node 0) are summed in fixed segments of SP_SEG sorted rows, one block
+// per segment, into partial rows folded in segment order (sp_seg_fold) --
+// the dense path's scheme (nodesum.cu) with a sparse scatter.
+constexpr int SP_SEG = 2048;
+
+__global__ void sp_seg_sum_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col,
+                                  const float *__restrict__ val, int d, const int *__restrict__ perm,
+                                  const int *__restrict__ off, const int *__restrict__ segoff,
+                                  const int *__restrict__ msegoff, const int *__restrict__ nseg, int K,
+                                  double *__restrict__ S, double *__restrict__ P) {
+    const int s = blockIdx.x;
+    if (s >= segoff[K]) return;
+    int lo = 0, hi = K;   // b = the node owning global segment s
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (segoff[mid] <= s) lo = mid; else hi = mid - 1;
+    }
+    int b = lo;
+    while (b + 1 <= K && segoff[b + 1] <= s) ++b;
+    const int sub = s - segoff[b];
+    const int r0 = off[b] + sub * SP_SEG, r1 = min(off[b + 1], r0 + SP_SEG);
+    double *dst = nseg[b] > 1 ? P + (int64_t)(msegoff[b] + sub) * d : S + (int64_t)b * d;
+    for (int t = r0; t < r1; ++t) {
         const int i = perm[t];
-        for (int64_t e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x) sb[col[e]] += (double)val[e];
+        for (int64_t e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x) dst[col[e]] += (double)val[e];
         __syncthreads();
     }
 }
 
-int node_bucket_sort(const int *bmu, int64_t n, int K, void *ws, const int **perm, const int **off, double *cnt,
-                     cudaStream_t st);
+__global__ void sp_seg_fold(const double *__restrict__ P, const int *__restrict__ msegoff,
+                            const int *__restrict__ nseg, int d, double *__restrict__ S) {
+    const int b = blockIdx.y;
+    const int ns = nseg[b];
+    if (ns <= 1) return;
+    const double *p = P + (int64_t)msegoff[b] * d;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < d; k += gridDim.x * blockDim.x) {
+        double a = 0.0;
+        for (int q = 0; q < ns; ++q) a += p[(int64_t)q * d + k];
+        S[(int64_t)b * d + k] = a;
+    }
+}
 
 }  // namespace somb
 
@@ -231,7 +260,16 @@ extern "C" int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col, 
     if (rc) return rc;
     if (n == 0) return SOMB_OK;
     if (row_order) cudaMemcpyAsync(row_order, perm, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, st);
-    sp_node_sums_kernel<<<K, 256, 0, st>>>(rowptr, col, val, d, perm, off, K, S);
+    int *nseg, *segoff, *msegoff;
+    double *P;
+    size_t P_doubles;
+    node_seg_plan(ws, n, d, K, SP_SEG, &nseg, &segoff, &msegoff, &P, &P_doubles, st);
+    const size_t need = ((size_t)(n + SP_SEG - 1) / SP_SEG * 2 + 2) * (size_t)d;
+    cudaMemsetAsync(P, 0, (need < P_doubles ? need : P_doubles) * sizeof(double), st);
+    const unsigned maxseg = (unsigned)(K + (n + SP_SEG - 1) / SP_SEG);
+    sp_seg_sum_kernel<<<maxseg, 256, 0, st>>>(rowptr, col, val, d, perm, off, segoff, msegoff, nseg, K, S, P);
+    note_launch();
+    sp_seg_fold<<<dim3((d + 255) / 256 < 64 ? (d + 255) / 256 : 64, K), 256, 0, st>>>(P, msegoff, nseg, d, S);
     note_launch();
     SOMB_LAUNCH_CHECK("node_sums_sparse");
     return SOMB_OK;
