@@ -14,21 +14,9 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
                      float wcoef, const float *thr0, int *cand, int *ccount, int *flags, float *dump,
                      unsigned *ctrs, OvfPool pool, int *ovf_head, float *ovf_lim, cudaStream_t st);
 
-// BMU workspace: cand [n][CAP] int | ccount [n] int | thr0 [n] float |
-// counters | overflow: head [2n] int, lim [2n] float, next [C], cnt [C],
-// entries [C][32] int2 with C = max(4096, n / 4) chunks.
-struct BmuWs {
-    int *cand, *ccount;
-    float *thr0;
-    unsigned *ctrs;
-    int *ovf_head;
-    float *ovf_lim;
-    OvfPool pool;
-};
-
 static unsigned ovf_chunks(int64_t n) { return (unsigned)(n / 4 > 4096 ? n / 4 : 4096); }
 
-static BmuWs bmu_carve(void *ws, int64_t n, size_t *total = nullptr) {
+BmuWs bmu_carve(void *ws, int64_t n, size_t *total) {
     BmuWs w;
     char *p = (char *)ws;
     auto take = [&](size_t bytes) { char *r = p; p += align_up(bytes, 256); return r; };

@@ -72,6 +72,19 @@ struct OvfPool {
     unsigned nchunks;   // 0 = no pool (truncate when full)
 };
 
+// BMU workspace (bmu.cu): cand [n][CAP] int | ccount [n] int | thr0 [n]
+// float | counters | overflow: head [2n] int, lim [2n] float, next [C],
+// cnt [C], entries [C][32] int2 with C = max(4096, n / 4) chunks.
+struct BmuWs {
+    int *cand, *ccount;
+    float *thr0;
+    unsigned *ctrs;     // [0] screen lockstep, [1] overflow chunks allocated
+    int *ovf_head;
+    float *ovf_lim;
+    OvfPool pool;
+};
+BmuWs bmu_carve(void *ws, int64_t n, size_t *total = nullptr);
+
 template <int CAP>
 struct CandRow {
     float rmin, thr, capbelow, win;

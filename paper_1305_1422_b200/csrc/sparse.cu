@@ -16,6 +16,7 @@ namespace somb {
 
 constexpr int SP_WARPS = 8;
 constexpr int SP_NNZ_BUF = 256;      // staged (col, val) pairs per warp
+constexpr int SP_CAP = 32;           // candidates in shared memory per row before spilling to the pool
 
 // dT[k][j] = fp32(w_jk - mu_k) for j < K, 0 for padding (prepare-time transpose)
 __global__ void sp_transpose(const float *__restrict__ W, const float *__restrict__ mu, int K, int d, int kp,
@@ -52,26 +53,34 @@ __global__ void __launch_bounds__(32 * SP_WARPS)
 sp_screen_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col, const float *__restrict__ val,
                  int64_t n, const float *__restrict__ dT, int kp, const float *__restrict__ c,
                  const float *__restrict__ xnorm, const float *__restrict__ scal, float wcoef,
-                 int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags) {
+                 int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags, OvfPool pool,
+                 int *__restrict__ ovf_head, float *__restrict__ ovf_lim) {
     __shared__ int s_col[SP_WARPS][SP_NNZ_BUF];
     __shared__ float s_val[SP_WARPS][SP_NNZ_BUF];
-    __shared__ float s_bv[SP_WARPS][SOMB_CAND_CAP];
-    __shared__ int s_bi[SP_WARPS][SOMB_CAND_CAP];
+    __shared__ float s_bv[SP_WARPS][SP_CAP];
+    __shared__ int s_bi[SP_WARPS][SP_CAP];
     const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * SP_WARPS + w;
     if (row >= n) return;
     const int64_t e0 = rowptr[row], e1 = rowptr[row + 1];
     const int nnz = (int)(e1 - e0);
     const float nmax = scal[1];
-    CandRow<SOMB_CAND_CAP> st;   // meaningful in lane 0 only
+    CandRow<SP_CAP> st;   // meaningful in lane 0 only
     cand_init(st, wcoef * (float)(nnz + 2) * xnorm[row] * nmax + ldexpf(scal[4], -21));
     const CandBuf cb{smem_addr(&s_bv[w][0]), smem_addr(&s_bi[w][0]), 4u};
     float thr = st.thr;
     for (int j0 = 0; j0 < kp; j0 += 256) {
+        const int jl = j0 + lane * 8;
+        const float4 *cp = reinterpret_cast<const float4 *>(c + jl);
+        const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
+        // a chunk of masked nodes (padding, or rows bit-identical to node 0:
+        // c = +inf, prep.cu) can never hold the BMU -- skip its gather
+        const bool fin = fminf(fminf(fminf(c0.x, c0.y), fminf(c0.z, c0.w)),
+                               fminf(fminf(c1.x, c1.y), fminf(c1.z, c1.w))) < INFINITY;
+        if (!__any_sync(0xffffffffu, fin)) continue;
         float acc[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
-        const int jl = j0 + lane * 8;
         for (int b0 = 0; b0 < nnz; b0 += SP_NNZ_BUF) {
             const int m = min(SP_NNZ_BUF, nnz - b0);
             __syncwarp();
@@ -90,8 +99,6 @@ sp_screen_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col
                 acc[6] = fmaf(v, b.z, acc[6]); acc[7] = fmaf(v, b.w, acc[7]);
             }
         }
-        const float4 *cp = reinterpret_cast<const float4 *>(c + jl);
-        float4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
         float r[8] = {fmaf(-2.0f, acc[0], c0.x), fmaf(-2.0f, acc[1], c0.y), fmaf(-2.0f, acc[2], c0.z),
                       fmaf(-2.0f, acc[3], c0.w), fmaf(-2.0f, acc[4], c1.x), fmaf(-2.0f, acc[5], c1.y),
                       fmaf(-2.0f, acc[6], c1.z), fmaf(-2.0f, acc[7], c1.w)};
@@ -105,15 +112,18 @@ sp_screen_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     float vq = __shfl_sync(0xffffffffu, r[q], src);
-                    if (lane == 0 && vq <= st.thr) cand_push<SOMB_CAND_CAP>(st, vq, j0 + src * 8 + q, cb);
+                    if (lane == 0 && vq <= st.thr) cand_push<SP_CAP>(st, vq, j0 + src * 8 + q, cb, pool);
                 }
             }
             thr = __shfl_sync(0xffffffffu, st.thr, 0);
         }
     }
     if (lane == 0) {
-        ccount[row] = cand_emit<SOMB_CAND_CAP>(st, cb, cand + row * SOMB_CAND_CAP);
+        ccount[row] = cand_emit<SP_CAP>(st, cb, cand + row * SOMB_CAND_CAP);
         flags[row] = st.trunc;
+        ovf_head[2 * row] = st.head;          // one column group: slot 1 stays empty
+        ovf_head[2 * row + 1] = -1;
+        ovf_lim[2 * row] = st.rmin + st.win;
     }
 }
 
@@ -123,6 +133,7 @@ __global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *
                                  const float *__restrict__ val, int64_t n, int d, const float *__restrict__ W,
                                  const double *__restrict__ w2, int K, const double *__restrict__ x2,
                                  const int *__restrict__ cand, const int *__restrict__ ccount, int all,
+                                 OvfPool pool, const int *__restrict__ ovf_head, const float *__restrict__ ovf_lim,
                                  int *__restrict__ bmu, double *__restrict__ d2min) {
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -134,9 +145,8 @@ __global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *
     double best = INFINITY;
     int bestj = 0x7fffffff;
     const double xx = x2[row];
-    for (int q = 0; q < cnt; ++q) {
-        const int j = scan ? q : cand[row * SOMB_CAND_CAP + q];
-        if ((unsigned)j >= (unsigned)K) continue;
+    auto eval = [&](int j) {
+        if ((unsigned)j >= (unsigned)K) return;
         const float *wr = W + (int64_t)j * d;
         double s = 0.0;
         for (int64_t e = e0 + lane; e < e1; e += 32) s = __fma_rn((double)val[e], (double)wr[col[e]], s);
@@ -145,6 +155,20 @@ __global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *
         if (v < best || (v == best && j < bestj)) {
             best = v;
             bestj = j;
+        }
+    };
+    for (int q = 0; q < cnt; ++q) eval(scan ? q : cand[row * SOMB_CAND_CAP + q]);
+    if (!scan) {   // spilled candidates (the screen's overflow chunks within the final window)
+        const float lim = ovf_lim[2 * row];
+        for (int c = ovf_head[2 * row]; c >= 0; c = pool.next[c]) {
+            const int m = pool.cnt[c];
+            const int2 e = lane < m ? pool.ent[(size_t)c * kOvfChunk + lane] : make_int2(0x7f800000, -1);
+            unsigned bal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(e.x) <= lim);
+            while (bal) {
+                const int src = __ffs(bal) - 1;
+                bal &= bal - 1u;
+                eval(__shfl_sync(0xffffffffu, e.y, src));
+            }
         }
     }
     if (lane == 0) {
@@ -233,17 +257,19 @@ extern "C" int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const 
     SOMB_REQUIRE(K > 0 && d > 0 && kp % 256 == 0, SOMB_E_INPUT, "bmu_sparse: bad shape");
     if (n == 0) return SOMB_OK;
     cudaStream_t st = as_stream(stream);
-    int *cand = (int *)ws;
-    int *ccount = (int *)((char *)ws + align_up((size_t)n * SOMB_CAND_CAP * sizeof(int), 256));
+    BmuWs w = bmu_carve(ws, n);
+    int *cand = w.cand, *ccount = w.ccount;
     if (!exact) {
+        cudaMemsetAsync(w.ctrs, 0, 2 * sizeof(unsigned), st);
         sp_screen_kernel<<<(unsigned)((n + SP_WARPS - 1) / SP_WARPS), 32 * SP_WARPS, 0, st>>>(
-            rowptr, col, val, n, dT, kp, c, xnorm, scal, window_coef, cand, ccount, flags);
+            rowptr, col, val, n, dT, kp, c, xnorm, scal, window_coef, cand, ccount, flags, w.pool, w.ovf_head,
+            w.ovf_lim);
         note_launch();
     } else {
         cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
     }
     sp_rerank_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(rowptr, col, val, n, d, W, w2, K, x2, cand, ccount,
-                                                              exact, bmu, d2min);
+                                                              exact, w.pool, w.ovf_head, w.ovf_lim, bmu, d2min);
     note_launch();
     SOMB_LAUNCH_CHECK("bmu_sparse");
     return SOMB_OK;
