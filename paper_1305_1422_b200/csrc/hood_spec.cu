@@ -329,26 +329,9 @@ struct MidEp {
         Nh[(((int64_t)pr * g.F + f) * nyo + yl) * D + d] = v;
     }
 };
-// inv for the count channel: den_j, with the exact zero pattern restored --
-// every nonzero influence is >= hmin (cutoff, or 1 for bubble), so a true
-// den_j is 0 or >= hmin, while the DFT rounding is orders of magnitude below
-// hmin / 2.
-struct DenB {
-    SpecGeom g; const double *Nh; int nyo, Dp1;
-    __device__ double operator()(int yl, int q2, int) const {
-        int plane = q2 >= g.F, f = q2 - plane * g.F;
-        return Nh[(((int64_t)plane * g.F + f) * nyo + yl) * Dp1 + (Dp1 - 1)];
-    }
-};
-struct DenEp {
-    SpecGeom g; int y0, j0, j1; double tau; double *den;
-    __device__ void operator()(int yl, int c, int, double v) const {
-        if (c >= g.nx) return;
-        int j = (y0 + yl) * g.nx + c;
-        if (j < j0 || j >= j1) return;
-        den[j] = v < tau ? 0.0 : v;
-    }
-};
+// den_j (spec_den_kernel) keeps the exact zero pattern: every nonzero
+// influence is >= hmin (cutoff, or 1 for bubble), so a true den_j is 0 or
+// >= hmin, while the DFT rounding is orders of magnitude below hmin / 2.
 // inv: num_y [nx x D] = Psi [nx x 2F] * [Nr_y; Ni_y]
 struct InvA {
     const double *psi; int F2;
@@ -380,6 +363,24 @@ struct InvEp {
         Wnew[o] = w;
     }
 };
+
+// den channel of the inverse DFT (N = 1: a GEMV, one thread per output;
+// running it through the 64-wide GEMM tile wasted 63/64 of the MMAs).
+__global__ void spec_den_kernel(SpecGeom g, const double *__restrict__ psi, const double *__restrict__ Nh, int nyo,
+                                int Dp1, int y0, int j0, int j1, double tau, double *__restrict__ den) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nyo * g.nx) return;
+    const int yl = e / g.nx, c = e % g.nx;
+    const int j = (y0 + yl) * g.nx + c;
+    if (j < j0 || j >= j1) return;
+    const int F2 = 2 * g.F;
+    double v = 0.0;
+    for (int q2 = 0; q2 < F2; ++q2) {
+        const int plane = q2 >= g.F, f = q2 - plane * g.F;
+        v = __fma_rn(psi[(int64_t)c * F2 + q2], Nh[(((int64_t)plane * g.F + f) * nyo + yl) * Dp1 + (Dp1 - 1)], v);
+    }
+    den[j] = v < tau ? 0.0 : v;
+}
 
 static SpecGeom spec_geom(const somb_map *m) {
     SpecGeom g;
@@ -439,8 +440,10 @@ int spec_update(const somb_map *m, const double *htab, const double *S, const do
     dgemm_launch(g.ny, 2 * g.F, nc, g.nx, FwdA{phi, g.nx}, FwdB{g, S, cnt, d}, FwdEp{g, Sh, Dp1}, st);
     dgemm_launch(g.F, 2 * nyo, nc, 2 * g.ny, MidA{g, ktT, nkeys, y0, nyo}, MidB{g, Sh, Dp1}, MidEp{g, Nh, nyo, Dp1},
                  st);
-    if (den_mode)
-        dgemm_launch(nyo, g.nx, 1, 2 * g.F, InvA{psi, 2 * g.F}, DenB{g, Nh, nyo, Dp1}, DenEp{g, y0, j0, j1, tau, den}, st);
+    if (den_mode) {
+        spec_den_kernel<<<(nyo * g.nx + 255) / 256, 256, 0, st>>>(g, psi, Nh, nyo, Dp1, y0, j0, j1, tau, den);
+        note_launch();
+    }
     dgemm_launch(nyo, g.nx, d, 2 * g.F, InvA{psi, 2 * g.F}, InvB{g, Nh, nyo, Dp1},
                  InvEp{g, y0, j0, j1, d, den, scale, 1.0 - scale, Wold, Wnew, num_out}, st);
     SOMB_LAUNCH_CHECK("spectral hood update");
