@@ -355,12 +355,11 @@ def run_ours(args):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         te = float(te.item())
         e2e = {"value": n * K * args.e2e_epochs / te, "unit": UNIT,
-               "h2d_bytes_per_step": int((count * SPARSE_NNZ * 8 + (count + 1) * 8 if sparse else count * d * 4)
-                                         + K * d * 4),
+               "h2d_bytes_per_step": int(count * SPARSE_NNZ * 8 + (count + 1) * 8 if sparse else count * d * 4),
                "d2h_bytes_per_step": int(K * d * 4 + n * 2 * 4 + K * 4),
-               "step": f"one public train() call: H2D of the rank's rows from pinned memory, "
-                       f"{args.e2e_epochs} epochs, final naive BMU pass, U-matrix, D2H of "
-                       f"codebook + BMU table + U-matrix",
+               "step": f"one public train() call: H2D of the rank's rows from pinned memory, seeded "
+                       f"codebook init (on device, numpy-identical), {args.e2e_epochs} epochs, final naive "
+                       f"BMU pass, U-matrix, D2H of codebook + BMU table + U-matrix",
                "seconds": te}
 
     cpu = None

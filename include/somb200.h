@@ -112,6 +112,14 @@ SOMB_API int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const f
                           float *c, double *w2, float *scal, void *ws,
                           void *stream);
 
+/* ---- codebook initialisation (train.py:164-166) ----------------------
+ * out[i] = numpy.random.default_rng(seed).random(count, dtype=float32)[i],
+ * bit for bit: PCG64 with the 128-bit state/increment numpy derives from
+ * the seed (numpy.random.PCG64(seed).state), XSL-RR output, float i from the
+ * 32-bit half i%2 of 64-bit output i/2, (u >> 8) * 2^-24. */
+SOMB_API int somb_uniform_f32(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                              int64_t count, float *out, void *stream);
+
 /* ---- BMU search (kernels.py:195-205 / 182-192, :407) -----------------
  * fp16 tensor-core screen (tcgen05, TMEM accumulators, TMA-staged tiles)
  * keeping per row every node within the screening window (<= CAP, the

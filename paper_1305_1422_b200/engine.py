@@ -58,6 +58,62 @@ def _round_up(v: int, a: int) -> int:
     return (v + a - 1) // a * a
 
 
+_STAGE = {}   # device index -> two cached page-locked staging halves
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device -> host copy through two cached page-locked staging buffers: the
+    D2H of chunk i+1 overlaps the host copy of chunk i (a pageable copy of the
+    160 MB cfg2 codebook runs at ~2 GB/s, and pinning a fresh buffer per call
+    costs more than the copy)."""
+    t = t.contiguous()
+    out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    nbytes = t.numel() * t.element_size()
+    if nbytes == 0:
+        return out
+    chunk = 16 << 20
+    dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
+    bufs = _STAGE.get(dev)
+    if bufs is None:
+        bufs = _STAGE[dev] = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    src = t.view(-1).view(torch.uint8)
+    dst = out.reshape(-1).view(np.uint8)
+    stream = torch.cuda.current_stream(t.device)
+    events = [None, None]
+    offs = list(range(0, nbytes, chunk))
+    for i, o in enumerate(offs + [None]):
+        if o is not None:   # enqueue D2H of chunk i into half i % 2
+            m = min(chunk, nbytes - o)
+            bufs[i % 2][:m].copy_(src[o:o + m], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            events[i % 2] = ev
+        if i > 0:           # host copy of chunk i - 1 while chunk i is in flight
+            p = offs[i - 1]
+            m = min(chunk, nbytes - p)
+            events[(i - 1) % 2].synchronize()
+            _host_copy(dst.ctypes.data + p, bufs[(i - 1) % 2].data_ptr(), m)
+    return out
+
+
+_POOL = None
+
+
+def _host_copy(dst: int, src: int, nbytes: int, parts: int = 4) -> None:
+    """memcpy split over threads (ctypes.memmove releases the GIL)."""
+    global _POOL
+    if nbytes < (4 << 20):
+        C.memmove(dst, src, nbytes)
+        return
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(parts)
+    step = -(-nbytes // parts)
+    futs = [_POOL.submit(C.memmove, dst + o, src + o, min(step, nbytes - o)) for o in range(0, nbytes, step)]
+    for f in futs:
+        f.result()
+
+
 def pick_device(device=None) -> torch.device:
     if not torch.cuda.is_available():
         raise errors.DeviceError("no CUDA device: somb200 runs only on a B200 (sm_100a)")
@@ -198,8 +254,16 @@ class SomEngine:
             raise errors.CodebookShapeMismatch(f"codebook {tuple(w.shape)}, expected {(self.K, self.d)}")
         self.W[: self.K].copy_(w.to(self.dev, non_blocking=True))
 
+    def init_codebook_device(self, seed: int):
+        """W = numpy.random.default_rng(seed).random((K, d), float32), generated
+        on the device bit for bit (train.py:164-166; somb_uniform_f32)."""
+        st = np.random.PCG64(seed).state["state"]
+        s, inc, m64 = int(st["state"]), int(st["inc"]), (1 << 64) - 1
+        _lib.call("somb_uniform_f32", s >> 64, s & m64, inc >> 64, inc & m64, self.K * self.d, _ptr(self.W),
+                  _stream(self.dev))
+
     def codebook(self) -> np.ndarray:
-        return self.W[: self.K].cpu().numpy()
+        return to_host(self.W[: self.K])
 
     # ------------------------------------------------------------- phases
     def prepare(self):
@@ -325,11 +389,20 @@ class SomEngine:
         dist.all_reduce(t, group=self.group)
         return int(t.item())
 
+    def bmu_coords(self) -> np.ndarray:
+        """(n, 2) int32 [row, col] of ALL rows' BMUs (rank order), computed on
+        the device (kernels.py:257-262) and copied through pinned memory."""
+        if self.world == 1:
+            b = self.bmu[: self.n]
+            return to_host(torch.stack((b // self.nx, b % self.nx), dim=1).to(torch.int32))
+        from .kernels import _to_coords
+        return _to_coords(self.gather_bmus(), self.nx)
+
     def gather_bmus(self) -> np.ndarray:
         """Flat BMU indices of ALL rows (rank order), on every rank."""
         local = self.bmu[: self.n].to(torch.int64)
         if self.world == 1:
-            return local.cpu().numpy()
+            return to_host(local)
         import torch.distributed as dist
         counts = [torch.zeros(1, dtype=torch.int64, device=self.dev) for _ in range(self.world)]
         dist.all_gather(counts, torch.tensor([self.n], dtype=torch.int64, device=self.dev),

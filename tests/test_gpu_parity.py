@@ -374,3 +374,15 @@ def test_bmu_search_one_call_matches_phases():
               _ptr(bmu), _ptr(d2), _ptr(eng.flags), _ptr(eng.ws), _stream(eng.dev))
     torch.cuda.synchronize()
     assert torch.equal(bmu[: eng.n], ref_b) and torch.equal(d2[: eng.n], ref_d)
+
+
+@pytest.mark.parametrize("seed,nx,ny,d", [(1, 7, 9, 1), (0, 20, 16, 31), (12345, 50, 40, 100), (1, 200, 200, 1000)])
+def test_device_codebook_init_bit_exact(seed, nx, ny, d):
+    """somb_uniform_f32 == numpy default_rng(seed).random((K, d), float32)
+    (train.py:164-166), so train() can initialise the codebook on the GPU."""
+    from paper_1305_1422_b200.engine import SomEngine
+    x = np.zeros((4, d), dtype=np.float32)
+    eng = SomEngine(x, nx, ny, S.MapType.PLANAR, device="cuda:0")
+    eng.init_codebook_device(seed)
+    ref = np.random.default_rng(seed).random((nx * ny, d), dtype=np.float32)
+    np.testing.assert_array_equal(eng.codebook(), ref)

@@ -152,3 +152,41 @@ def test_fileio_roundtrip(tmp_path):
     nx, ny, w2 = fileio.load_codebook(str(tmp_path / "a.wts"))
     assert (nx, ny) == (3, 2)
     np.testing.assert_allclose(w2, w, rtol=1e-5)
+
+
+def _pcg64_floats(seed, start, count):
+    """Restatement of csrc/rng.cu: PCG64 jump-ahead to output start//2, then
+    the numpy float32 construction (u >> 8) * 2^-24 from 32-bit halves."""
+    st = np.random.PCG64(seed).state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    mult, mask = 0x2360ED051FC65DA44385DF649FCCF645, (1 << 128) - 1
+
+    def advance(state, delta):
+        acc_m, acc_p, cur_m, cur_p = 1, 0, mult, inc
+        while delta:
+            if delta & 1:
+                acc_m, acc_p = (acc_m * cur_m) & mask, (acc_p * cur_m + cur_p) & mask
+            cur_p, cur_m = ((cur_m + 1) * cur_p) & mask, (cur_m * cur_m) & mask
+            delta >>= 1
+        return (acc_m * state + acc_p) & mask
+
+    k = start // 2
+    s = advance(s, k)
+    out = []
+    while len(out) < count + (start % 2):
+        s = (s * mult + inc) & mask
+        hi, lo = s >> 64, s & ((1 << 64) - 1)
+        v, r = hi ^ lo, s >> 122
+        o = ((v >> r) | (v << ((64 - r) & 63))) & ((1 << 64) - 1)
+        out += [np.float32((o & 0xFFFFFFFF) >> 8) * np.float32(2.0 ** -24),
+                np.float32((o >> 32) >> 8) * np.float32(2.0 ** -24)]
+    return np.array(out[start % 2: start % 2 + count], dtype=np.float32)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 12345])
+def test_device_init_restatement_matches_numpy(seed):
+    """The jump-ahead used by somb_uniform_f32 reproduces numpy's
+    default_rng(seed).random(float32) at arbitrary offsets (train.py:164-166)."""
+    ref = np.random.default_rng(seed).random(5000, dtype=np.float32)
+    for start, count in [(0, 17), (1, 9), (2048, 33), (4095, 7), (4990, 10)]:
+        np.testing.assert_array_equal(_pcg64_floats(seed, start, count), ref[start:start + count])
