@@ -233,6 +233,9 @@ SOMB_API int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const fl
 /* S (K x d, fp64, dense) / cnt from CSR rows; ws >= somb_node_sums_ws(n, d, K).
  * Nodes with more than 2048 rows are summed in 2048-row segments folded in
  * segment order (the dense path's scheme), else in ascending row order. */
+/* Workspace of somb_bmu_sparse (the lockstep screen keeps each row's window
+ * state and candidate buffer between codebook slabs). */
+SOMB_API size_t somb_bmu_sparse_ws(int64_t n);
 SOMB_API int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col,
                                    const float *val, int64_t n, int32_t d,
                                    const int32_t *bmu, int32_t K, double *S,

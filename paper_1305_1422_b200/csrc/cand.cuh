@@ -85,6 +85,19 @@ struct BmuWs {
 };
 BmuWs bmu_carve(void *ws, int64_t n, size_t *total = nullptr);
 
+// The same buffer in global memory (one row's slots contiguous): lets a
+// row's candidate state persist across kernel phases (sparse lockstep screen).
+struct CandBufG {
+    float *v;
+    int *i;
+};
+__device__ __forceinline__ float cb_ldv(const CandBufG &b, int e) { return b.v[e]; }
+__device__ __forceinline__ int cb_ldi(const CandBufG &b, int e) { return b.i[e]; }
+__device__ __forceinline__ void cb_st(const CandBufG &b, int e, float v, int j) {
+    b.v[e] = v;
+    b.i[e] = j;
+}
+
 template <int CAP>
 struct CandRow {
     float rmin, thr, capbelow, win;

@@ -127,6 +127,132 @@ sp_screen_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col
     }
 }
 
+// ------------------------------------------------- lockstep sparse screen
+// The gather above is DRAM-bound: every row sweeps the whole transposed
+// codebook (2 GB at cfg3), so concurrently running rows touch it at random
+// and L2 hits are ~5% (profiles/).  Here the node loop is OUTSIDE: all
+// warps sweep one 128-node slab of dT (K-chunk, 25.6 MB at cfg3) over their
+// rows before moving to the next, a global counter keeping them within LAG
+// slabs of each other, so the slab is served from L2.  Each row's window
+// state and candidate buffer persist in global memory between slabs; the
+// row's nonzeros are re-staged per slab (2 KB, 1/64 of the gathered bytes).
+// Semantics (window, visiting order, spill, emit) equal sp_screen_kernel.
+constexpr int SPL_CH = 128;          // nodes per slab (4 per lane)
+
+struct SpRowState {
+    float rmin, thr, capbelow, win;
+    int cnt, trunc, head, pad;
+};
+
+__device__ __forceinline__ void sp_state_load(CandRow<SP_CAP> &st, const SpRowState &g) {
+    st.rmin = g.rmin; st.thr = g.thr; st.capbelow = g.capbelow; st.win = g.win;
+    st.cnt = g.cnt; st.trunc = g.trunc; st.head = g.head;
+}
+__device__ __forceinline__ void sp_state_store(const CandRow<SP_CAP> &st, SpRowState &g) {
+    g.rmin = st.rmin; g.thr = st.thr; g.capbelow = st.capbelow; g.win = st.win;
+    g.cnt = st.cnt; g.trunc = st.trunc; g.head = st.head;
+}
+
+__global__ void __launch_bounds__(32 * SP_WARPS)
+sp_screen_ls_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col, const float *__restrict__ val,
+                    int64_t n, const float *__restrict__ dT, int kp, const float *__restrict__ c,
+                    const float *__restrict__ xnorm, const float *__restrict__ scal, float wcoef,
+                    int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags, OvfPool pool,
+                    int *__restrict__ ovf_head, float *__restrict__ ovf_lim, SpRowState *__restrict__ rs,
+                    float *__restrict__ gbv, int *__restrict__ gbi, unsigned *__restrict__ done_ctr, int lag) {
+    __shared__ int s_col[SP_WARPS][SP_NNZ_BUF];
+    __shared__ float s_val[SP_WARPS][SP_NNZ_BUF];
+    const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * SP_WARPS + w, GW = (int64_t)gridDim.x * SP_WARPS;
+    const float nmax = scal[1];
+    if (lane == 0) {
+        for (int64_t row = gw; row < n; row += GW) {
+            CandRow<SP_CAP> st;
+            const int nnz = (int)(rowptr[row + 1] - rowptr[row]);
+            cand_init(st, wcoef * (float)(nnz + 2) * xnorm[row] * nmax + ldexpf(scal[4], -21));
+            sp_state_store(st, rs[row]);
+        }
+    }
+    const int NC = kp / SPL_CH;
+    for (int ci = 0; ci < NC; ++ci) {
+        if (lane == 0 && ci > lag) {   // soft lockstep over the slabs (lag slabs ahead at most)
+            const unsigned need = (unsigned)GW * (unsigned)(ci - lag);
+            for (int spin = 0; spin < (1 << 22); ++spin) {
+                unsigned cur;
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(done_ctr) : "memory");
+                if (cur >= need) break;
+                __nanosleep(128);
+            }
+        }
+        __syncwarp();
+        const int j0 = ci * SPL_CH;
+        const int jl = j0 + lane * 4;
+        const float4 c4 = __ldg(reinterpret_cast<const float4 *>(c + jl));
+        const bool fin = fminf(fminf(c4.x, c4.y), fminf(c4.z, c4.w)) < INFINITY;
+        if (__any_sync(0xffffffffu, fin)) {   // a slab of masked nodes cannot hold a BMU
+#pragma unroll 1
+            for (int64_t row = gw; row < n; row += GW) {
+                CandRow<SP_CAP> st;
+                if (lane == 0) sp_state_load(st, rs[row]);
+                float thr = __shfl_sync(0xffffffffu, lane == 0 ? st.thr : 0.0f, 0);
+                const int64_t e0 = rowptr[row], e1 = rowptr[row + 1];
+                const int nnz = (int)(e1 - e0);
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int b0 = 0; b0 < nnz; b0 += SP_NNZ_BUF) {
+                    const int m = min(SP_NNZ_BUF, nnz - b0);
+                    __syncwarp();
+                    for (int t = lane; t < m; t += 32) {
+                        s_col[w][t] = col[e0 + b0 + t];
+                        s_val[w][t] = val[e0 + b0 + t];
+                    }
+                    __syncwarp();
+#pragma unroll 8
+                    for (int t = 0; t < m; ++t) {
+                        const float v = s_val[w][t];
+                        const float4 a = __ldg(reinterpret_cast<const float4 *>(dT + (int64_t)s_col[w][t] * kp + jl));
+                        acc[0] = fmaf(v, a.x, acc[0]); acc[1] = fmaf(v, a.y, acc[1]);
+                        acc[2] = fmaf(v, a.z, acc[2]); acc[3] = fmaf(v, a.w, acc[3]);
+                    }
+                }
+                float r[4] = {fmaf(-2.0f, acc[0], c4.x), fmaf(-2.0f, acc[1], c4.y), fmaf(-2.0f, acc[2], c4.z),
+                              fmaf(-2.0f, acc[3], c4.w)};
+                const float lo = fminf(fminf(r[0], r[1]), fminf(r[2], r[3]));
+                unsigned hit = __ballot_sync(0xffffffffu, lo <= thr);
+                if (hit) {
+                    const CandBufG cb{gbv + row * SP_CAP, gbi + row * SP_CAP};
+                    while (hit) {   // ascending node order; lane 0 owns the row state
+                        const int src = __ffs(hit) - 1;
+                        hit &= hit - 1;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float vq = __shfl_sync(0xffffffffu, r[q], src);
+                            if (lane == 0 && vq <= st.thr) cand_push<SP_CAP>(st, vq, j0 + src * 4 + q, cb, pool);
+                        }
+                    }
+                    if (lane == 0) sp_state_store(st, rs[row]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(done_ctr, 1u);
+        }
+    }
+    if (lane == 0) {
+        for (int64_t row = gw; row < n; row += GW) {
+            CandRow<SP_CAP> st;
+            sp_state_load(st, rs[row]);
+            const CandBufG cb{gbv + row * SP_CAP, gbi + row * SP_CAP};
+            ccount[row] = cand_emit<SP_CAP>(st, cb, cand + row * SOMB_CAND_CAP);
+            flags[row] = st.trunc;
+            ovf_head[2 * row] = st.head;
+            ovf_head[2 * row + 1] = -1;
+            ovf_lim[2 * row] = st.rmin + st.win;
+        }
+    }
+}
+
 // Exact fp64 re-rank with the reference's sparse formula:
 // d2 = (x2 - 2 sum_t v_t w_j[col_t]) + w2_j, clamp >= 0 (kernels.py:216-219).
 __global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col,
@@ -260,10 +386,38 @@ extern "C" int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const 
     BmuWs w = bmu_carve(ws, n);
     int *cand = w.cand, *ccount = w.ccount;
     if (!exact) {
-        cudaMemsetAsync(w.ctrs, 0, 2 * sizeof(unsigned), st);
-        sp_screen_kernel<<<(unsigned)((n + SP_WARPS - 1) / SP_WARPS), 32 * SP_WARPS, 0, st>>>(
-            rowptr, col, val, n, dT, kp, c, xnorm, scal, window_coef, cand, ccount, flags, w.pool, w.ovf_head,
-            w.ovf_lim);
+        cudaMemsetAsync(w.ctrs, 0, 4 * sizeof(unsigned), st);
+        static int ls = -1, lag = 0;   // SOMB_SPARSE_LOCKSTEP=0: row-at-a-time gather; SOMB_SPARSE_LAG (0 = slab barrier, measured best)
+        if (ls < 0) {
+            const char *e = getenv("SOMB_SPARSE_LOCKSTEP");
+            ls = e ? atoi(e) != 0 : 1;
+            const char *l = getenv("SOMB_SPARSE_LAG");
+            if (l) lag = atoi(l);
+        }
+        if (ls && kp % SPL_CH == 0) {
+            size_t base = 0;
+            bmu_carve(nullptr, n, &base);
+            char *p = (char *)ws + base;
+            SpRowState *rs = (SpRowState *)p;
+            p += align_up((size_t)n * sizeof(SpRowState), 256);
+            float *gbv = (float *)p;
+            p += align_up((size_t)n * SP_CAP * sizeof(float), 256);
+            int *gbi = (int *)p;
+            int dev = 0, sms = kSmCount, per_sm = 1;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sp_screen_ls_kernel, 32 * SP_WARPS, 0);
+            if (per_sm < 1) per_sm = 1;
+            const int64_t need = (n + SP_WARPS - 1) / SP_WARPS;
+            const unsigned grid = (unsigned)(need < (int64_t)per_sm * sms ? need : (int64_t)per_sm * sms);
+            sp_screen_ls_kernel<<<grid, 32 * SP_WARPS, 0, st>>>(rowptr, col, val, n, dT, kp, c, xnorm, scal,
+                                                               window_coef, cand, ccount, flags, w.pool, w.ovf_head,
+                                                               w.ovf_lim, rs, gbv, gbi, w.ctrs + 2, lag);
+        } else {
+            sp_screen_kernel<<<(unsigned)((n + SP_WARPS - 1) / SP_WARPS), 32 * SP_WARPS, 0, st>>>(
+                rowptr, col, val, n, dT, kp, c, xnorm, scal, window_coef, cand, ccount, flags, w.pool, w.ovf_head,
+                w.ovf_lim);
+        }
         note_launch();
     } else {
         cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
@@ -299,4 +453,10 @@ extern "C" int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col, 
     note_launch();
     SOMB_LAUNCH_CHECK("node_sums_sparse");
     return SOMB_OK;
+}
+
+extern "C" size_t somb_bmu_sparse_ws(int64_t n) {
+    size_t base = 0;
+    bmu_carve(nullptr, n, &base);
+    return base + align_up((size_t)n * sizeof(SpRowState), 256) + 2 * align_up((size_t)n * SP_CAP * 4, 256) + 256;
 }

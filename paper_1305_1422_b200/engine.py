@@ -137,6 +137,8 @@ def dist_info(group=None):
 class SomEngine:
     """Resident dataset slice + codebook + buffers for one GPU (one rank)."""
 
+    _sparse = False   # SparseEngine: CSR rows, gather screen (larger BMU workspace)
+
     def __init__(self, data, n_columns: int, n_rows: int, map_type: MapType,
                  grid: GridType = GridType.RECTANGULAR, device=None, group=None,
                  options: Optional[EngineOptions] = None):
@@ -183,7 +185,8 @@ class SomEngine:
         if self.opt.hypot_table and grid is GridType.RECTANGULAR:
             self.dist_tab = torch.from_numpy(distance_table(self.nx, self.ny, map_type)).to(dev)
         lib = _lib.load()
-        ws = max(lib.somb_codebook_ws(self.K, d), lib.somb_bmu_ws(n),
+        ws = max(lib.somb_codebook_ws(self.K, d),
+                 lib.somb_bmu_sparse_ws(n) if self._sparse else lib.somb_bmu_ws(n),
                  lib.somb_node_sums_ws(n, d, self.K),
                  lib.somb_hood_ws(C.byref(self.cmap), self.K, d), 1 << 16)
         self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)

@@ -23,6 +23,8 @@ _SPARSE_WINDOW = 4.0 * 2.0 ** -24
 
 
 class SparseEngine(SomEngine):
+    _sparse = True
+
     def _init_data(self, data):
         if not isinstance(data, SparseDataset):
             raise errors.KernelDataMismatch("SparseEngine needs a SparseDataset")
