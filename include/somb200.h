@@ -120,6 +120,18 @@ SOMB_API int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const f
 SOMB_API int somb_uniform_f32(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                               int64_t count, float *out, void *stream);
 
+/* 2-pass split screen operands (screen_impl 3): the fp16 hi copy plus the
+ * fp8 (e4m3) cross-term operands, 2 dp bytes per row -- X8 = [e4m3(xh / 32)
+ * | e4m3(xl * 32)], W8 = [e4m3(wl * 32) | e4m3(wh / 32)] with xl, wl the
+ * fp16 residuals; scaling puts max|hi| <= 2^13 (xexp = 13 - exponent of
+ * max|x - nu|).  The tensor-core screen computes hi.hi (kind::f16) +
+ * x_hi8.w_lo8 + x_lo8.w_hi8 (kind::f8f6f4, twice the fp16 rate). */
+SOMB_API int somb_data_pack_f8(const float *X, int64_t n, int32_t d, const float *nu, int32_t xexp,
+                               uint16_t *Xh, uint8_t *X8, int32_t dp, float *xnorm, double *x2, void *stream);
+SOMB_API int somb_codebook_prepare_f8(const float *W, int32_t K, int32_t d, const float *nu, int32_t xexp,
+                                      uint16_t *Wh, uint8_t *W8, int32_t dp, int32_t kp, float *c,
+                                      double *w2, float *scal, void *ws, void *stream);
+
 /* ---- BMU search (kernels.py:195-205 / 182-192, :407) -----------------
  * fp16 tensor-core screen (tcgen05, TMEM accumulators, TMA-staged tiles)
  * keeping per row every node within the screening window (<= CAP, the
@@ -127,7 +139,9 @@ SOMB_API int somb_uniform_f32(uint64_t state_hi, uint64_t state_lo, uint64_t inc
  * the candidates with the reference formula `dist_mode`, first-minimum
  * ties.  Output bmu int32[n], d2min fp64[n] (clamped >= 0), flags int32[n]
  * (bit0 = window truncated).  ws >= somb_bmu_ws(n).  screen_impl: 0 =
- * tcgen05 (sm_100a), 1 = SIMT reference screen (tests). */
+ * tcgen05 (sm_100a), 1 = SIMT reference screen (tests), 2 = none (exact
+ * scan), 3 = tcgen05 2-pass split (Xl / Wl = the fp8 operands of
+ * somb_data_pack_f8 / somb_codebook_prepare_f8). */
 SOMB_API int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xnorm,
                    const double *x2, int64_t n, int32_t d, int32_t dp,
                    const uint16_t *Wh, const float *W, const float *c,
@@ -152,7 +166,7 @@ SOMB_API int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const float
 SOMB_API int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm,
                                     int64_t n, int32_t dp, const uint16_t *Wh, const uint16_t *Wl,
                                     const float *c, int32_t kp, const float *scal,
-                                    float window_coef, float *dump, void *ws,
+                                    float window_coef, int32_t passes, float *dump, void *ws,
                                     void *stream);
 /* row_order (may be NULL): a permutation of [0, n) giving the order in
  * which rows are re-ranked -- the rows sorted by their previous BMU

@@ -54,7 +54,9 @@ SIGNATURES = {
     "somb_bmu_dense": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P, P, I32, I32, P, F32,
                                  I32, I32, P, P, P, P, P]),
     "somb_bmu_screen": (C.c_int, [P, P, P, I64, I32, P, P, P, I32, I32, P, F32, P, I32, P, P, P]),
-    "somb_debug_screen_dump": (C.c_int, [P, P, P, I64, I32, P, P, P, I32, P, F32, P, P, P]),
+    "somb_debug_screen_dump": (C.c_int, [P, P, P, I64, I32, P, P, P, I32, P, F32, I32, P, P, P]),
+    "somb_data_pack_f8": (C.c_int, [P, I64, I32, P, I32, P, P, I32, P, P, P]),
+    "somb_codebook_prepare_f8": (C.c_int, [P, I32, I32, P, I32, P, P, I32, I32, P, P, P, P, P]),
     "somb_bmu_rerank": (C.c_int, [P, P, I64, I32, P, P, I32, I32, I32, P, P, P, P, P, P]),
     "somb_bmu_search": (C.c_int, [P, P, P, P, P, I64, I32, I32, P, P, P, P, P, I32, I32, P, F32, P, P, I32,
                                   I32, P, P, P, P, P]),

@@ -5,6 +5,8 @@
 // operands (prep.cu); the re-rank evaluates the reference formula in fp64
 // from the original f32 rows, so the returned BMU is the reference's argmin
 // whenever it lies in the screened candidate set.
+#include <cuda_fp8.h>
+
 #include "cand.cuh"
 
 namespace somb {
@@ -12,7 +14,7 @@ namespace somb {
 int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh,
                      const __half *Wl, int kp, const float *c, const float *xnorm, const float *scal,
                      float wcoef, const float *thr0, int *cand, int *ccount, int *flags, float *dump,
-                     unsigned *ctrs, OvfPool pool, int *ovf_head, float *ovf_lim, cudaStream_t st);
+                     unsigned *ctrs, OvfPool pool, int *ovf_head, float *ovf_lim, int passes, cudaStream_t st);
 
 static unsigned ovf_chunks(int64_t n) { return (unsigned)(n / 4 > 4096 ? n / 4 : 4096); }
 
@@ -54,11 +56,20 @@ struct OvfView {
 // 3-pass mode (Xl, Wl given): the seed is the fp64 value of the same split
 // product, and the slack is 1.5 windows (the tensor-core value differs from
 // it by at most the screen error, <= half a window).
+__device__ __forceinline__ double e4m3_to_double(uint8_t b) {
+    __nv_fp8_e4m3 v;
+    v.__x = b;
+    return (double)(float)v;
+}
+
+// f8 = 1: Xl / Wl hold the fp8 cross operands [x_hi8 | x_lo8], [w_lo8 | w_hi8]
+// (2 dp bytes per row, 2-pass screen): the seed is the fp64 value of the same
+// hi.hi + cross products, slack 1.5 windows as for the 3-pass screen.
 __global__ void screen_seed_kernel(const __half *__restrict__ Xh, const __half *__restrict__ Xl, int64_t n, int dp,
                                    const __half *__restrict__ Wh, const __half *__restrict__ Wl, int K,
                                    const float *__restrict__ c, const float *__restrict__ xnorm,
                                    const float *__restrict__ scal, float wcoef, const int *__restrict__ prev,
-                                   float *__restrict__ thr0) {
+                                   float *__restrict__ thr0, int f8) {
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -69,7 +80,19 @@ __global__ void screen_seed_kernel(const __half *__restrict__ Xh, const __half *
         const __half2 *w = reinterpret_cast<const __half2 *>(Wh + (int64_t)j * dp);
         float win = wcoef * xnorm[row] * scal[1];
         float r;
-        if (Xl == nullptr) {
+        if (f8) {
+            const uint8_t *x8 = reinterpret_cast<const uint8_t *>(Xl) + row * (int64_t)(2 * dp);
+            const uint8_t *w8 = reinterpret_cast<const uint8_t *>(Wl) + (int64_t)j * (2 * dp);
+            double acc = 0.0;
+            for (int k = lane; k < dp; k += 32) {
+                acc += (double)__half2float(Xh[row * (int64_t)dp + k]) * (double)__half2float(Wh[(int64_t)j * dp + k]);
+                acc += e4m3_to_double(x8[k]) * e4m3_to_double(w8[k]) +
+                       e4m3_to_double(x8[dp + k]) * e4m3_to_double(w8[dp + k]);
+            }
+            acc = warp_sum(acc);
+            r = (float)(acc * (double)scal[0] + (double)c[j]);
+            if (r < FLT_MAX) r += 1.5f * win;
+        } else if (Xl == nullptr) {
             float acc = 0.0f;
             for (int k = lane; k < dp / 2; k += 32) {
                 float2 a = __half22float2(x[k]), b = __half22float2(w[k]);
@@ -569,7 +592,8 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
                                const float *scal, float window_coef, const int32_t *prev_bmu,
                                int32_t screen_impl, int32_t *flags, void *ws, void *stream) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % 256 == 0, SOMB_E_INPUT, "bmu_screen: dp=%d kp=%d", dp, kp);
-    SOMB_REQUIRE(screen_impl >= 0 && screen_impl <= 2, SOMB_E_CONFIG, "bad screen_impl %d", screen_impl);
+    SOMB_REQUIRE(screen_impl >= 0 && screen_impl <= 3, SOMB_E_CONFIG, "bad screen_impl %d", screen_impl);
+    SOMB_REQUIRE(screen_impl != 3 || (Xl && Wl), SOMB_E_INPUT, "bmu_screen: the fp8 split screen needs Xl / Wl");
     if (n == 0 || screen_impl == 2) return SOMB_OK;
     cudaStream_t st = as_stream(stream);
     BmuWs w = bmu_carve(ws, n);
@@ -577,16 +601,18 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
     float *thr0 = nullptr;
     if (prev_bmu) {
         thr0 = w.thr0;
-        const bool three = Xl != nullptr && Wl != nullptr && screen_impl == 0;
+        const bool split = Xl != nullptr && Wl != nullptr && (screen_impl == 0 || screen_impl == 3);
         screen_seed_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(
-            (const __half *)Xh, three ? (const __half *)Xl : nullptr, n, dp, (const __half *)Wh,
-            three ? (const __half *)Wl : nullptr, K, c, xnorm, scal, window_coef, prev_bmu, thr0);
+            (const __half *)Xh, split ? (const __half *)Xl : nullptr, n, dp, (const __half *)Wh,
+            split ? (const __half *)Wl : nullptr, K, c, xnorm, scal, window_coef, prev_bmu, thr0,
+            screen_impl == 3);
         note_launch();
     }
-    if (screen_impl == 0)
+    if (screen_impl == 0 || screen_impl == 3)
         return launch_screen_tc((const __half *)Xh, (const __half *)Xl, n, dp, (const __half *)Wh,
                                 (const __half *)Wl, kp, c, xnorm, scal, window_coef, thr0, cand, ccount, flags,
-                                nullptr, w.ctrs, w.pool, w.ovf_head, w.ovf_lim, st);
+                                nullptr, w.ctrs, w.pool, w.ovf_head, w.ovf_lim,
+                                screen_impl == 3 ? 2 : (Xl && Wl ? 3 : 1), st);
     unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
     screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh, kp, c,
                                                       xnorm, scal, window_coef, thr0, cand, ccount, flags);
@@ -612,7 +638,7 @@ extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int3
         const char *e = getenv("SOMB_RERANK_PIPE");
         g_rerank_pipe = e ? atoi(e) != 0 : 1;
     }
-    int all = screen_impl == 2, split = screen_impl == 0;
+    int all = screen_impl == 2, split = screen_impl == 0 || screen_impl == 3;
     OvfView ov{nullptr, nullptr, nullptr, nullptr, nullptr};
     if (split) ov = OvfView{bw.ovf_head, bw.ovf_lim, bw.pool.ent, bw.pool.next, bw.pool.cnt};
     if (all) cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
@@ -680,13 +706,14 @@ extern "C" int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws
 // computed as usual.  Used to measure the real screen error.
 extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm, int64_t n,
                                       int32_t dp, const uint16_t *Wh, const uint16_t *Wl, const float *c, int32_t kp,
-                                      const float *scal, float window_coef, float *dump, void *ws, void *stream) {
+                                      const float *scal, float window_coef, int32_t passes, float *dump, void *ws,
+                                      void *stream) {
     int64_t m = n < 128 ? n : 128;
     BmuWs w = bmu_carve(ws, n);
     int *flags = (int *)w.thr0;
     return launch_screen_tc((const __half *)Xh, (const __half *)Xl, m, dp, (const __half *)Wh, (const __half *)Wl, kp,
                             c, xnorm, scal, window_coef, nullptr, w.cand, w.ccount, flags, dump, w.ctrs, w.pool,
-                            w.ovf_head, w.ovf_lim, as_stream(stream));
+                            w.ovf_head, w.ovf_lim, passes, as_stream(stream));
 }
 
 

@@ -8,6 +8,8 @@
 // r_ij; both operands are centred, which keeps the fp16 rounding error small
 // relative to the gaps between nodes after the codebook collapses
 // (SURVEY.md 7.3-1).
+#include <cuda_fp8.h>
+
 #include "common.cuh"
 
 namespace somb {
@@ -93,6 +95,47 @@ __global__ void data_pack_kernel(const float *__restrict__ X, int64_t n, int d,
     }
 }
 
+// 2-pass (fp16 + fp8 cross terms) operands: Xh = fp16(v 2^xexp) (xexp puts
+// max |v| 2^xexp <= 2^13), X8 = [e4m3(xh / 32) | e4m3(xl * 32)] with the
+// residual xl = v 2^xexp - xh (2 dp bytes per row), so that
+// x_hi8 . w_lo8 + x_lo8 . w_hi8 ~ xh . wl + xl . wh in the fp16 pass's units.
+__device__ __forceinline__ uint8_t to_e4m3(double v) {
+    return (uint8_t)__nv_cvt_float_to_fp8((float)v, __NV_SATFINITE, __NV_E4M3);
+}
+
+__global__ void data_pack_f8_kernel(const float *__restrict__ X, int64_t n, int d, const float *__restrict__ nu,
+                                    int xexp, __half *__restrict__ Xh, uint8_t *__restrict__ X8, int dp,
+                                    float *__restrict__ xnorm, double *__restrict__ x2) {
+    int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const float *x = X + row * d;
+    __half *o = Xh + row * dp;
+    uint8_t *o8 = X8 + row * (int64_t)(2 * dp);
+    const double sc = ldexp(1.0, xexp);
+    double nrm = 0.0, sq = 0.0;
+    for (int k = lane; k < dp; k += 32) {
+        double v = 0.0;
+        if (k < d) {
+            double xv = (double)x[k];
+            v = xv - (double)nu[k];
+            nrm += v * v;
+            sq += xv * xv;
+        }
+        const __half h = __double2half(v * sc);
+        const double hd = (double)__half2float(h);
+        o[k] = h;
+        o8[k] = to_e4m3(hd * (1.0 / 32.0));
+        o8[dp + k] = to_e4m3((v * sc - hd) * 32.0);
+    }
+    nrm = warp_sum(nrm);
+    sq = warp_sum(sq);
+    if (lane == 0) {
+        xnorm[row] = (float)sqrt(nrm);
+        x2[row] = sq;
+    }
+}
+
 // ------------------------------------------------------------- codebook prep
 // ws layout: mu f32[d] | mu_nu f64[d] | stats f32[4] {nmax, dabsmax, -, -}
 __global__ void cb_colmean(const float *__restrict__ W, int K, int d, const float *__restrict__ nu,
@@ -153,22 +196,35 @@ __global__ void cb_rowstats(const float *__restrict__ W, int K, int d, const flo
     }
 }
 
-__device__ __forceinline__ int pick_exp(float amax) {
-    // largest e with amax * 2^e <= 2^14 (fp16 max 65504); 0 for amax == 0
+__device__ __forceinline__ int pick_exp(float amax, int top = 14) {
+    // largest e with amax * 2^e <= 2^top (fp16 max 65504; top 13 for the
+    // fp8 cross-term ranges); 0 for amax == 0
     if (!(amax > 0.0f)) return 0;
     int e;
     frexpf(amax, &e);           // amax = f * 2^e, f in [0.5, 1)
-    return 14 - e;
+    return top - e;
 }
 
+// W8 (2-pass mode, Wl unused): [e4m3(wl * 32) | e4m3(wh / 32)], 2 dp bytes per row
 __global__ void cb_pack(const float *__restrict__ W, int K, int d, const float *__restrict__ mu,
                         int xexp, __half *__restrict__ Wh, __half *__restrict__ Wl, int dp, int kp,
                         float *__restrict__ c, const float *__restrict__ stats,
-                        float *__restrict__ scal) {
+                        float *__restrict__ scal, uint8_t *__restrict__ W8) {
     int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     int lane = threadIdx.x & 31;
     if (j >= kp) return;
-    int sexp = pick_exp(stats[1]);
+    int sexp = pick_exp(stats[1], W8 ? 13 : 14);
+    if (W8) {
+        uint8_t *o8 = W8 + (int64_t)j * (2 * dp);
+        const float *w = W + (int64_t)(j < K ? j : 0) * d;
+        const double sc = ldexp(1.0, sexp);
+        for (int k = lane; k < dp; k += 32) {
+            const double v = (j < K && k < d) ? ((double)w[k] - (double)mu[k]) * sc : 0.0;
+            const double hd = (double)__half2float(__double2half(v));
+            o8[k] = to_e4m3((v - hd) * 32.0);
+            o8[dp + k] = to_e4m3(hd * (1.0 / 32.0));
+        }
+    }
     __half *o = Wh ? Wh + (int64_t)j * dp : nullptr;
     __half *ol = Wl ? Wl + (int64_t)j * dp : nullptr;
     if (o == nullptr) {
@@ -258,9 +314,45 @@ extern "C" int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const
     note_launch();
     cb_rowstats<<<(K + 7) / 8, 256, 0, st>>>(W, K, d, mu, mu_nu, c, w2, nrm, stats);
     note_launch();
-    cb_pack<<<(kp + 7) / 8, 256, 0, st>>>(W, K, d, mu, xexp, (__half *)Wh, (__half *)Wl, dp, kp, c, stats, scal);
+    cb_pack<<<(kp + 7) / 8, 256, 0, st>>>(W, K, d, mu, xexp, (__half *)Wh, (__half *)Wl, dp, kp, c, stats, scal,
+                                          nullptr);
     // (Wh may be NULL: the sparse path screens against a transposed fp32 copy)
     note_launch();
     SOMB_LAUNCH_CHECK("somb_codebook_prepare");
+    return SOMB_OK;
+}
+
+extern "C" int somb_data_pack_f8(const float *X, int64_t n, int32_t d, const float *nu, int32_t xexp, uint16_t *Xh,
+                                 uint8_t *X8, int32_t dp, float *xnorm, double *x2, void *stream) {
+    SOMB_REQUIRE(d > 0 && dp >= d && dp % 8 == 0 && Xh && X8, SOMB_E_INPUT, "data_pack_f8: bad pitch d=%d dp=%d", d,
+                 dp);
+    if (n == 0) return SOMB_OK;
+    int64_t blocks = (n + 7) / 8;
+    data_pack_f8_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(X, n, d, nu, xexp, (__half *)Xh, X8, dp,
+                                                                         xnorm, x2);
+    note_launch();
+    SOMB_LAUNCH_CHECK("somb_data_pack_f8");
+    return SOMB_OK;
+}
+
+extern "C" int somb_codebook_prepare_f8(const float *W, int32_t K, int32_t d, const float *nu, int32_t xexp,
+                                        uint16_t *Wh, uint8_t *W8, int32_t dp, int32_t kp, float *c, double *w2,
+                                        float *scal, void *ws, void *stream) {
+    SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && dp % 8 == 0 && kp >= K && kp % 256 == 0 && Wh && W8,
+                 SOMB_E_INPUT, "codebook_prepare_f8: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
+    cudaStream_t st = as_stream(stream);
+    char *p = (char *)ws;
+    float *mu = (float *)p;            p += align_up((size_t)d * sizeof(float), 256);
+    double *mu_nu = (double *)p;       p += align_up((size_t)d * sizeof(double), 256);
+    float *nrm = (float *)p;           p += align_up((size_t)K * sizeof(float), 256);
+    float *stats = (float *)p;
+    cudaMemsetAsync(stats, 0, 4 * sizeof(float), st);
+    cb_colmean<<<(d + 7) / 8, 256, 0, st>>>(W, K, d, nu, mu, mu_nu);
+    note_launch();
+    cb_rowstats<<<(K + 7) / 8, 256, 0, st>>>(W, K, d, mu, mu_nu, c, w2, nrm, stats);
+    note_launch();
+    cb_pack<<<(kp + 7) / 8, 256, 0, st>>>(W, K, d, mu, xexp, (__half *)Wh, nullptr, dp, kp, c, stats, scal, W8);
+    note_launch();
+    SOMB_LAUNCH_CHECK("somb_codebook_prepare_f8");
     return SOMB_OK;
 }

@@ -41,6 +41,12 @@ constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_THREADS = 32 * (2 + TC_EPI_WARPS);
 constexpr int TC_ROWS = 128;                      // data rows per CTA (TMEM lanes)
 
+// PASSES = 2: fp16 hi.hi plus the two cross terms hi.lo + lo.hi on the fp8
+// (e4m3) tensor path at twice the fp16 rate: per tile, first the fp8 stages
+// A8 = [x_hi8 | x_lo8] . B8 = [w_lo8 | w_hi8] (2 dp fp8 features, 128 per
+// stage, accumulated from zero so their reduced-precision accumulation is
+// relative to the small cross terms), then the fp16 stages on top
+// (~2 fp16-pass equivalents instead of 3; error ~0.2 window units).
 // PASSES = 1: fp16 operands; PASSES = 3: split operands (hi + lo residual),
 // D += hi.hi + hi.lo + lo.hi (~22-bit operand precision, 3x the MMAs) for
 // small feature counts where the 1-pass fp16 window holds too many
@@ -185,6 +191,27 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint
     }
 }
 
+// kind::f8f6f4 (e4m3 x e4m3, f32 accumulate): K = 32 per op; the instruction
+// descriptor bits equal the f16 one (a/b format 0 = E4M3, c format F32)
+template <int CG>
+__device__ __forceinline__ void tc_mma_f8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    if constexpr (CG == 1) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+}
+
 // K-major, SWIZZLE_128B smem matrix descriptor: 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     uint64_t d = 0;
@@ -305,6 +332,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
     const int iters = first_in_cluster < num_units ? (num_units - first_in_cluster + unit_step - 1) / unit_step : 0;
     const int NT = kp / TC_BN;
     const int KB = (dp + TC_BK - 1) / TC_BK;
+    const int KB8 = PASSES == 2 ? (2 * dp + 127) / 128 : 0;   // fp8 cross-term stages (128 features each)
 
     if (warp == 0) {
         if (lane == 0) {
@@ -332,6 +360,22 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         }
                     }
                     const int node0 = nt * TC_BN + Cfg::B_ROWS * (int)crank;
+                    for (int kb = 0; kb < KB8; ++kb) {   // PASSES == 2: fp8 cross terms first
+                        mbar_wait(empty0 + 8 * stage, phase ^ 1);
+                        const uint32_t fb = full0 + 8 * stage;
+                        if (leader) mbar_expect_tx(fb, CG * Cfg::STAGE_BYTES);
+                        uint8_t *st0 = smem + stage * Cfg::STAGE_BYTES;
+                        tma_load_2d<CG>(smem_u32(st0), map_xl, fb, kb * 128, row0);
+                        if constexpr (MC == 1) {
+                            tma_load_2d<CG>(smem_u32(st0 + Cfg::A_BYTES), map_wl, fb, kb * 128, node0);
+                        } else {
+                            const uint32_t sub = (uint32_t)pair * (Cfg::B_BYTES / MC);
+                            const uint16_t mcm = (uint16_t)((1u << crank) | (1u << (crank + 2)));
+                            tma_load_2d_mc(smem_u32(st0 + Cfg::A_BYTES + sub), map_wl, fb, kb * 128,
+                                           node0 + (Cfg::B_ROWS / MC) * (int)pair, mcm);
+                        }
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                    }
                     for (int kb = 0; kb < KB; ++kb) {
                         mbar_wait(empty0 + 8 * stage, phase ^ 1);
                         const uint32_t fb = full0 + 8 * stage;
@@ -385,6 +429,18 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     mbar_wait(tempty0 + 8 * acc, aphase ^ 1);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TC_BN);
+                    for (int kb = 0; kb < KB8; ++kb) {   // fp8 cross terms, accumulated from zero
+                        mbar_wait(full0 + 8 * stage, phase);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                        const uint32_t b0 = a0 + Cfg::A_BYTES;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            tc_mma_f8<CG>(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), Cfg::IDESC,
+                                          (kb | k) != 0);
+                        tc_commit<CG>(empty0 + 8 * stage, MC == 1 ? (uint16_t)0x3 : (uint16_t)0xF);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                    }
                     for (int kb = 0; kb < KB; ++kb) {
                         mbar_wait(full0 + 8 * stage, phase);
                         tc_fence_after();
@@ -393,7 +449,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
 #pragma unroll
                         for (int k = 0; k < TC_BK / TC_UMMA_K; ++k) {
                             tc_mma_f16<CG>(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), Cfg::IDESC,
-                                           (kb | k) != 0);
+                                           (KB8 > 0 || (kb | k) != 0) ? 1u : 0u);
                             if constexpr (PASSES == 3) {
                                 const uint32_t al = b0 + Cfg::B_BYTES, bl = al + Cfg::A_BYTES;
                                 tc_mma_f16<CG>(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(bl + 32 * k), Cfg::IDESC, 1);
@@ -552,14 +608,18 @@ static EncodeTiledFn get_encode() {
     return fn;
 }
 
-static int make_map(CUtensorMap *map, const void *base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+// 2-D K-major map with 128-byte inner boxes: fp16 (64 elements) or, with
+// u8 = true, fp8 bytes (128 elements)
+static int make_map(CUtensorMap *map, const void *base, uint64_t inner, uint64_t outer, uint32_t box_outer,
+                    bool u8 = false) {
     EncodeTiledFn enc = get_encode();
     SOMB_REQUIRE(enc, SOMB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {inner * 2};
-    cuuint32_t box[2] = {(cuuint32_t)TC_BK, box_outer};
+    cuuint64_t strides[1] = {inner * (u8 ? 1 : 2)};
+    cuuint32_t box[2] = {(cuuint32_t)(u8 ? 128 : TC_BK), box_outer};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+    CUresult r = enc(map, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                     const_cast<void *>(base), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     SOMB_REQUIRE(r == CUDA_SUCCESS, SOMB_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -602,7 +662,9 @@ static int screen_tc_init() {
     if (!rc) rc = set_smem(screen_tc2_kernel<3, 8>, TcCfg<2, 3, 8>::SMEM, "screen_tc2x3 smem");
     if (!rc) rc = set_smem(screen_tc2_kernel<3, 16>, TcCfg<2, 3, 16>::SMEM, "screen_tc2x3 smem");
     if (!rc) rc = set_smem(screen_tc2_kernel<3, 32>, TcCfg<2, 3, 32>::SMEM, "screen_tc2x3 smem");
+    if (!rc) rc = set_smem(screen_tc2_kernel<2, 32>, TcCfg<2, 2, 32>::SMEM, "screen_tc2x2 smem");
     if (!rc) rc = set_smem(screen_tc4_kernel<1, 32>, TcCfg<2, 1, 32>::SMEM, "screen_tc4 smem");
+    if (!rc) rc = set_smem(screen_tc4_kernel<2, 32>, TcCfg<2, 2, 32>::SMEM, "screen_tc4x2 smem");
     if (!rc) rc = set_smem(screen_tc4_kernel<3, 32>, TcCfg<2, 3, 32>::SMEM, "screen_tc4x3 smem");
     if (rc) return rc;
     init = true;
@@ -627,20 +689,29 @@ int screen_tc_set_knob(const char *key, int value) {
 int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh, const __half *Wl, int kp,
                      const float *c, const float *xnorm, const float *scal, float wcoef, const float *thr0, int *cand,
                      int *ccount, int *flags, float *dump, unsigned *ctrs, OvfPool pool, int *ovf_head,
-                     float *ovf_lim, cudaStream_t st) {
+                     float *ovf_lim, int passes, cudaStream_t st) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % TC_BN == 0, SOMB_E_INPUT, "screen_tc: dp %% 8 and kp %% 256 required");
     int rc0 = screen_tc_init();
     if (rc0) return rc0;
     const int cg = g_tc_group;
     // multicast variant: CTA pairs, full capacity, 1-pass (the 3-pass screen is
     // MMA-bound, and 4-CTA cluster packing can leave SMs idle)
-    const bool three = Xl != nullptr && Wl != nullptr;
-    const int mcv = cg == 2 && g_half_cap == 32 && !three ? g_mc : 1;
+    // passes: 1 (fp16), 2 (fp16 + fp8 cross terms; Xl / Wl hold the fp8
+    // operands, 2 dp bytes per row), 3 (fp16 hi/lo split)
+    SOMB_REQUIRE(passes >= 1 && passes <= 3 && (passes == 1 || (Xl && Wl)), SOMB_E_INPUT,
+                 "screen_tc: %d passes need the split operands", passes);
+    const bool three = passes == 3, two = passes == 2;
+    const int mcv = cg == 2 && g_half_cap == 32 && passes == 1 ? g_mc : 1;   // (2-pass with multicast measured slower)
     CUtensorMap mx, mw, mxl, mwl;
     int rc = make_map(&mx, Xh, (uint64_t)dp, (uint64_t)n, TC_ROWS);
     if (!rc) rc = make_map(&mw, Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg / mcv));
-    if (!rc) rc = make_map(&mxl, three ? Xl : Xh, (uint64_t)dp, (uint64_t)n, TC_ROWS);
-    if (!rc) rc = make_map(&mwl, three ? Wl : Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg / mcv));
+    if (two) {
+        if (!rc) rc = make_map(&mxl, Xl, (uint64_t)(2 * dp), (uint64_t)n, TC_ROWS, true);
+        if (!rc) rc = make_map(&mwl, Wl, (uint64_t)(2 * dp), (uint64_t)kp, (uint32_t)(TC_BN / cg / mcv), true);
+    } else {
+        if (!rc) rc = make_map(&mxl, three ? Xl : Xh, (uint64_t)dp, (uint64_t)n, TC_ROWS);
+        if (!rc) rc = make_map(&mwl, three ? Wl : Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg / mcv));
+    }
     if (rc) return rc;
     int dev = 0, sms = kSmCount;
     cudaGetDevice(&dev);
@@ -678,7 +749,10 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
     KERN<PV, HV><<<grid, TC_THREADS, TcCfg<CGV, PV, HV>::SMEM, st>>>(mx, mw, mxl, mwl, n, dp, kp, c, xnorm, scal, wcoef, \
                                                                      thr0, cand, ccount, flags, dump, ctr, lag, pool, \
                                                                      ovf_head, ovf_lim)
-    if (cg == 1) {
+    if (two) {
+        SOMB_REQUIRE(cg == 2, SOMB_E_CONFIG, "screen_tc: the fp8 split screen needs CTA pairs (tc_group 2)");
+        if (mcv == 2) SCREEN_LAUNCH(screen_tc4_kernel, 2, 2, 32); else SCREEN_LAUNCH(screen_tc2_kernel, 2, 2, 32);
+    } else if (cg == 1) {
         if (three) SCREEN_LAUNCH(screen_tc1_kernel, 1, 3, 16); else SCREEN_LAUNCH(screen_tc1_kernel, 1, 1, 16);
     } else if (mcv == 2) {
         if (three) SCREEN_LAUNCH(screen_tc4_kernel, 2, 3, 32); else SCREEN_LAUNCH(screen_tc4_kernel, 2, 1, 32);

@@ -40,8 +40,9 @@ class EngineOptions:
     window_kappa: float = _DEF_WINDOW_KAPPA
     hypot_table: bool = True          # numpy-hypot distances for rect grids (bit parity)
     seed_prev: bool = True            # seed the screen threshold from the previous BMUs
-    screen_passes: int = 0            # 0 auto (3 if the padded feature count <= 256), 1, or 3
+    screen_passes: int = 0            # 0 auto (2 if the padded feature count <= 256), 1, 2 (fp16 + fp8 cross terms) or 3
     window_kappa3: Optional[float] = None     # None: _kappa3(d)
+    window_kappa2: float = float(os.environ.get("SOMB_WINDOW_KAPPA2", "0.6"))   # 2-pass (fp16 + fp8) window: measured max error ~0.22 units (tools/f8_probe.py)
     conv: str = "auto"                # neighbourhood convolution: "auto", "direct", "spectral"
     rerank_order: bool = True         # re-rank rows in previous-BMU order (L2 locality; same result)
 
@@ -192,6 +193,8 @@ class SomEngine:
         self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)
         self.window_coef = self._window_coef()
         self.screen_impl = {"tensor": 0, "simt": 1, "exact": 2}[self.opt.screen]
+        if self.screen_impl == 0 and self.passes == 2:
+            self.screen_impl = 3       # tcgen05 fp16 + fp8 cross-term split screen
         self.has_prev = False
 
     # ------------------------------------------------------- subclass hooks
@@ -202,17 +205,28 @@ class SomEngine:
         self._upload_dense(x, dry=True)
         dp0 = _round_up(self.d, 8)
         p = self.opt.screen_passes
-        self.passes = 3 if (p == 3 or (p == 0 and dp0 <= 256)) and self.opt.screen == "tensor" else 1
+        if self.opt.screen != "tensor":
+            self.passes = 1
+        elif p in (1, 2, 3):
+            self.passes = p
+        else:
+            self.passes = 2 if dp0 <= 256 else 1
         self.pack_dataset()
 
     def _init_codebook_buffers(self):
         self.Wh = torch.empty((self.kp, self.dp), dtype=torch.float16, device=self.dev)
-        self.Wl = (torch.empty((self.kp, self.dp), dtype=torch.float16, device=self.dev)
-                   if self.passes == 3 else None)
+        if self.passes == 3:
+            self.Wl = torch.empty((self.kp, self.dp), dtype=torch.float16, device=self.dev)
+        elif self.passes == 2:     # fp8 cross operands [w_lo8 | w_hi8]
+            self.Wl = torch.empty((self.kp, 2 * self.dp), dtype=torch.uint8, device=self.dev)
+        else:
+            self.Wl = None
 
     def _window_coef(self) -> float:
         if self.passes == 3:
             kappa = self.opt.window_kappa3 if self.opt.window_kappa3 is not None else _kappa3(self.d)
+        elif self.passes == 2:
+            kappa = self.opt.window_kappa2
         else:
             kappa = self.opt.window_kappa
         return float(kappa * _U16 / math.sqrt(self.d))
@@ -241,14 +255,19 @@ class SomEngine:
         ws = torch.empty(int(lib.somb_data_stats_ws(d)), dtype=torch.uint8, device=dev)
         _lib.call("somb_data_stats", _ptr(self.X), n, d, _ptr(self.nu), _ptr(absmax), _ptr(ws), st)
         a = float(absmax.item())                 # one host sync per dataset
-        self.xexp = 0 if a <= 0.0 or not math.isfinite(a) else 14 - math.frexp(a)[1]
+        passes = getattr(self, "passes", 1)
+        top = 13 if passes == 2 else 14          # the fp8 cross operands need max|hi| <= 2^13
+        self.xexp = 0 if a <= 0.0 or not math.isfinite(a) else top - math.frexp(a)[1]
         self.Xh = torch.empty((max(n, 1), self.dp), dtype=torch.float16, device=dev)
-        self.Xl = (torch.empty((max(n, 1), self.dp), dtype=torch.float16, device=dev)
-                   if getattr(self, "passes", 1) == 3 else None)
+        self.Xl = None
+        if passes == 3:
+            self.Xl = torch.empty((max(n, 1), self.dp), dtype=torch.float16, device=dev)
+        elif passes == 2:
+            self.Xl = torch.empty((max(n, 1), 2 * self.dp), dtype=torch.uint8, device=dev)
         self.xnorm = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         self.x2 = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
-        _lib.call("somb_data_pack", _ptr(self.X), n, d, _ptr(self.nu), self.xexp, _ptr(self.Xh),
-                  _ptr(self.Xl), self.dp, _ptr(self.xnorm), _ptr(self.x2), st)
+        _lib.call("somb_data_pack_f8" if passes == 2 else "somb_data_pack", _ptr(self.X), n, d, _ptr(self.nu),
+                  self.xexp, _ptr(self.Xh), _ptr(self.Xl), self.dp, _ptr(self.xnorm), _ptr(self.x2), st)
 
     # ----------------------------------------------------------- codebook
     def set_codebook(self, w):
@@ -270,7 +289,8 @@ class SomEngine:
 
     # ------------------------------------------------------------- phases
     def prepare(self):
-        _lib.call("somb_codebook_prepare", _ptr(self.W), self.K, self.d, _ptr(self.nu), self.xexp,
+        _lib.call("somb_codebook_prepare_f8" if self.passes == 2 else "somb_codebook_prepare", _ptr(self.W),
+                  self.K, self.d, _ptr(self.nu), self.xexp,
                   _ptr(self.Wh), _ptr(self.Wl), self.dp, self.kp, _ptr(self.c), _ptr(self.w2),
                   _ptr(self.scal), _ptr(self.ws), _stream(self.dev))
 
@@ -317,7 +337,7 @@ class SomEngine:
         dump = torch.full((m, self.kp), float("nan"), dtype=torch.float32, device=self.dev)
         _lib.call("somb_debug_screen_dump", _ptr(self.Xh), _ptr(self.Xl), _ptr(self.xnorm), self.n,
                   self.dp, _ptr(self.Wh), _ptr(self.Wl), _ptr(self.c), self.kp, _ptr(self.scal),
-                  C.c_float(self.window_coef),
+                  C.c_float(self.window_coef), self.passes,
                   _ptr(dump), _ptr(self.ws), _stream(self.dev))
         return dump[:, : self.K]
 
@@ -325,7 +345,7 @@ class SomEngine:
         """Per-row candidate counts of the last screen (tcgen05 two-half encoding)."""
         off = ((self.n * _lib.CAND_CAP * 4 + 255) // 256) * 256
         cc = self.ws[off: off + 4 * self.n].view(torch.int32)
-        if self.screen_impl == 0:
+        if self.screen_impl in (0, 3):
             return (cc & 255) + ((cc >> 8) & 255)
         return cc
 

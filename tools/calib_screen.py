@@ -47,13 +47,13 @@ for e in range(E):
     rmin = r.min(1, keepdim=True).values
     out = [f"ep{e} r={st.radius:.1f}: max|err|/(u16 |x'| nmax/sqrt(D)) = {ratio:.2f}; "
            f"exact-argmin screen rank max {int(rank.max())}"]
-    for kappa in ((0.05, 0.1, 0.25, 0.5, 1.0) if eng.passes == 3 else (4, 8, 12, 16, 24)):
+    for kappa in ((0.05, 0.1, 0.25, 0.5, 1.0) if eng.passes in (2, 3) else (4, 8, 12, 16, 24)):
         w = kappa * scale[:, :1]
         cnt = (r <= rmin + w).sum(1).float()
         out.append(f"k{kappa}: mean {cnt.mean():.1f} max {int(cnt.max())}")
     print("; ".join(out), flush=True)
     eng.search()
-    cc = eng.candidate_counts().float()
+    cc = eng.candidate_counts()[:n].float()
     print(f"   full-N candidates/row mean {cc.mean():.2f} max {int(cc.max())}, "
           f"truncated {((eng.flags[:n] & 0xFFFF) != 0).float().mean():.3f}", flush=True)
     eng.epoch(st.radius, st.scale, 1e-3)

@@ -1,8 +1,8 @@
-"""Full-scale parity of the screened search: 10 cfg2 epochs on 1M rows with
+"""Full-scale parity of the screened search: 10 epochs of a bench config with
 the tcgen05 screen vs the exact fp64 scan (screen='exact'), same data, same
 initial codebook.  Reports codebook / U-matrix max relative error and the
 final BMU mismatches with their fp64 top-2 gaps.
-   python tools/full_parity.py [rows] [epochs]"""
+   python tools/full_parity.py [cfg] [rows] [epochs]"""
 import json
 import os
 import sys
@@ -12,16 +12,20 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
 import paper_1305_1422_b200 as S  # noqa: E402
 from paper_1305_1422_b200.engine import EngineOptions  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
-E = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+cfg_name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+n0, d, nx, ny, mt, grid, nbh, compact, desc = bench.CONFIGS[cfg_name]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else n0
+E = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 g = torch.Generator(device="cuda")
 g.manual_seed(1001)
-X = torch.rand((n, 1000), generator=g, device="cuda")
+X = torch.rand((n, d), generator=g, device="cuda")
 data = S.DenseDataset(X)
-cfg = S.TrainConfig(n_epochs=E, n_columns=200, n_rows=200, map_type=S.MapType.TOROID,
+cfg = S.TrainConfig(n_epochs=E, n_columns=nx, n_rows=ny, map_type=S.MapType(mt), grid=S.GridType(grid),
+                    neighborhood=S.Neighborhood(nbh), compact_support=compact,
                     kernel=S.Kernel.DENSE_BLOCKED, seed=1)
 out = {}
 for screen in ("tensor", "exact"):
@@ -32,8 +36,8 @@ for screen in ("tensor", "exact"):
 wt, bt, ut, _ = out["tensor"]
 we, be, ue, _ = out["exact"]
 rel = lambda a, b: float(np.max(np.abs(a.astype(np.float64) - b) / np.maximum(np.abs(b), 1e-12)))
-fb = bt[:, 0].astype(np.int64) * 200 + bt[:, 1]
-eb = be[:, 0].astype(np.int64) * 200 + be[:, 1]
+fb = bt[:, 0].astype(np.int64) * nx + bt[:, 1]
+eb = be[:, 0].astype(np.int64) * nx + be[:, 1]
 bad = np.flatnonzero(fb != eb)
 gap = None
 if len(bad):
@@ -42,8 +46,9 @@ if len(bad):
     d2 = (xs * xs).sum(1, keepdim=True) + (W * W).sum(1)[None] - 2 * xs @ W.T
     t2 = torch.topk(d2, 2, dim=1, largest=False).values
     gap = float(((t2[:, 1] - t2[:, 0]) / t2[:, 0]).max())
-res = {"rows": n, "epochs": E, "codebook_max_rel": rel(wt, we), "codebook_bit_identical_frac": float(np.mean(wt == we)),
-       "umatrix_max_rel": rel(ut, ue), "bmu_mismatch": int(len(bad)), "bmu_mismatch_max_gap": gap}
+res = {"config": desc, "rows": n, "epochs": E, "codebook_max_rel": rel(wt, we),
+       "codebook_bit_identical_frac": float(np.mean(wt == we)), "umatrix_max_rel": rel(ut, ue),
+       "bmu_mismatch": int(len(bad)), "bmu_mismatch_max_gap": gap}
 print(json.dumps(res))
 os.makedirs("gpurun_out", exist_ok=True)
-json.dump(res, open(f"gpurun_out/full_parity_{n}.json", "w"))
+json.dump(res, open(f"gpurun_out/full_parity_{cfg_name}_{n}.json", "w"))

@@ -15,15 +15,18 @@ from paper_1305_1422_b200.engine import SomEngine, _ptr, _stream  # noqa: E402
 
 warm = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-n, d, nx, ny = 1_000_000, 1000, 200, 200
+cfgn = sys.argv[3] if len(sys.argv) > 3 else "cfg2"
+passes = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+n, d, nx, ny, mt, grid, nbh, compact, _ = bench.CONFIGS[cfgn]
 g = torch.Generator(device="cuda")
 g.manual_seed(1001)
 X = torch.rand((n, d), generator=g, device="cuda")
-eng = SomEngine(X, nx, ny, S.MapType.TOROID)
-eng.set_codebook(S.init_codebook(S.TrainConfig(n_columns=nx, n_rows=ny, seed=1), d).weights)
+from paper_1305_1422_b200.engine import EngineOptions  # noqa: E402
+eng = SomEngine(X, nx, ny, S.MapType(mt), S.GridType(grid), options=EngineOptions(screen_passes=passes))
+eng.init_codebook_device(1)
 for e in range(warm):
-    r, sc = bench.schedule_for("cfg2", e)
-    eng.epoch(r, sc, 1e-3)
+    r, sc = bench.schedule_for(cfgn, e)
+    eng.epoch(r, sc, 1e-3, S.Neighborhood(nbh), compact)
 eng.prepare()
 lib = _lib.load()
 
@@ -37,7 +40,7 @@ def run(tag, **knobs):
         a.record()
         _lib.call("somb_bmu_screen", _ptr(eng.Xh), _ptr(eng.Xl), _ptr(eng.xnorm), eng.n, eng.dp, _ptr(eng.Wh),
                   _ptr(eng.Wl), _ptr(eng.c), eng.K, eng.kp, _ptr(eng.scal), C.c_float(eng.window_coef),
-                  _ptr(eng.bmu), 0, _ptr(eng.flags), _ptr(eng.ws), _stream(eng.dev))
+                  _ptr(eng.bmu), eng.screen_impl, _ptr(eng.flags), _ptr(eng.ws), _stream(eng.dev))
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
@@ -45,9 +48,11 @@ def run(tag, **knobs):
           f"-> {2.0 * n * nx * ny * d / (min(ts) / 1e3) / 1e12:.0f} TF/s", flush=True)
 
 
-for mc in (1, 2, 1, 2):
-    for lag in (8, 0, 16):
-        run(f"multicast {mc} lag {lag}", tc_multicast=mc, screen_lag=lag)
-run("mc2 lag 8 profile (no epilogue)", tc_multicast=2, screen_lag=8, screen_profile=1)
-run("mc1 lag 8 profile (no epilogue)", tc_multicast=1, screen_lag=8, screen_profile=1)
-run("back to normal", tc_multicast=2, screen_lag=8, screen_profile=0)
+if cfgn == "cfg2":
+    for mc in (1, 2, 1, 2):
+        for lag in (8, 0, 16):
+            run(f"multicast {mc} lag {lag}", tc_multicast=mc, screen_lag=lag)
+for lag in (8, 0):
+    run(f"{cfgn} passes {eng.passes} lag {lag}", screen_lag=lag)
+run(f"{cfgn} passes {eng.passes} profile (no epilogue)", screen_lag=8, screen_profile=1)
+run("back to normal", screen_lag=8, screen_profile=0)
