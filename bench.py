@@ -323,8 +323,8 @@ def run_ours(args):
     cand_stats = {"mean": float(cc.mean()), "p50": float(np.median(cc)), "p99": float(np.percentile(cc, 99)),
                   "max": float(cc.max())}
     flags = eng.flags[: eng.n].cpu().numpy()
-    trunc = float((((flags & 0xFF) | ((flags >> 8) & 0xFF)) & 1).astype(bool).mean()) if eng.n else 0.0
-    spilled = float((((flags & 0xFF) | ((flags >> 8) & 0xFF)) & 2).astype(bool).mean()) if eng.n else 0.0
+    trunc = float((((flags & 0xFF) | ((flags >> 8) & 0xFF) | ((flags >> 16) & 0xFF) | ((flags >> 24) & 0xFF)) & 1).astype(bool).mean()) if eng.n else 0.0
+    spilled = float((((flags & 0xFF) | ((flags >> 8) & 0xFF) | ((flags >> 16) & 0xFF) | ((flags >> 24) & 0xFF)) & 2).astype(bool).mean()) if eng.n else 0.0
 
     # end to end through the public API: host (pinned) data -> train() -> host results
     e2e = None

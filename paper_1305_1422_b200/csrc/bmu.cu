@@ -27,8 +27,8 @@ BmuWs bmu_carve(void *ws, int64_t n, size_t *total) {
     w.ccount = (int *)take((size_t)n * sizeof(int));
     w.thr0 = (float *)take((size_t)n * sizeof(float));
     w.ctrs = (unsigned *)take(4 * sizeof(unsigned));
-    w.ovf_head = (int *)take((size_t)2 * n * sizeof(int));
-    w.ovf_lim = (float *)take((size_t)2 * n * sizeof(float));
+    w.ovf_head = (int *)take((size_t)4 * n * sizeof(int));
+    w.ovf_lim = (float *)take((size_t)4 * n * sizeof(float));
     w.pool.next = (int *)take((size_t)C * sizeof(int));
     w.pool.cnt = (int *)take((size_t)C * sizeof(int));
     w.pool.ent = (int2 *)take((size_t)C * kOvfChunk * sizeof(int2));
@@ -40,11 +40,41 @@ BmuWs bmu_carve(void *ws, int64_t n, size_t *total) {
 
 // Spilled candidates of one row (tcgen05 screen overflow lists), read by the re-rank.
 struct OvfView {
-    const int *head;    // [2n], nullptr = no overflow lists
-    const float *lim;   // [2n] final window limit of each column group
+    const int *head;    // [4n] per (row, column group), nullptr = no overflow lists
+    const float *lim;   // [4n] final window limit of each column group
     const int2 *ent;
     const int *next, *cnt;
+    const unsigned *ngp;   // column groups of the tcgen05 lists (written by the screen)
 };
+
+// Candidate list of a row: one segment (SIMT screen) or NG column-group
+// segments (tcgen05 screen: count byte g, slots [g * 64 / NG, ...)).
+struct CandLayout {
+    int c[4];
+    int ng, gs, cnt;
+};
+__device__ __forceinline__ CandLayout cand_layout(int cc, int split, int ng) {
+    CandLayout L;
+    if (!split) {
+        L.ng = 1; L.gs = SOMB_CAND_CAP; L.c[0] = cc; L.c[1] = L.c[2] = L.c[3] = 0; L.cnt = cc;
+        return L;
+    }
+    L.ng = ng; L.gs = SOMB_CAND_CAP / ng; L.cnt = 0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        L.c[g] = g < ng ? (cc >> (8 * g)) & 255 : 0;
+        L.cnt += L.c[g];
+    }
+    return L;
+}
+__device__ __forceinline__ int cand_slot(const CandLayout &L, int q) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        if (q < L.c[g]) return g * L.gs + q;
+        q -= L.c[g];
+    }
+    return 0;
+}
 
 // Seed of each row's acceptance threshold from its previous BMU: the screened
 // value of that node (same fp16 operands, fp32 FMA) plus one window and an
@@ -205,9 +235,8 @@ __global__ void rerank_kernel(const float *__restrict__ X, const double *__restr
     // candidate list: one segment [0, cc) or, for the two-half tcgen05
     // epilogue, [0, cc & 255) and [CAP/2, CAP/2 + (cc >> 8 & 255))
     int cc = all ? 0 : ccount[row];
-    int c0 = split ? (cc & 255) : cc;
-    int c1 = split ? ((cc >> 8) & 255) : 0;
-    int cnt = c0 + c1;
+    const CandLayout L = cand_layout(cc, split, split && ov.ngp ? (int)*ov.ngp : 2);
+    int cnt = L.cnt;
     bool scan_all = all || cnt <= 0;
     if (scan_all) cnt = K;
     double best = INFINITY;
@@ -220,16 +249,16 @@ __global__ void rerank_kernel(const float *__restrict__ X, const double *__restr
     for (int q = 0;; ++q) {
         int j;
         if (q < cnt) {
-            j = scan_all ? q : cand[row * SOMB_CAND_CAP + (q < c0 ? q : SOMB_CAND_CAP / 2 + (q - c0))];
+            j = scan_all ? q : cand[row * SOMB_CAND_CAP + cand_slot(L, q)];
         } else {
             if (scan_all || ov.head == nullptr) break;
             while (ovbal == 0u) {     // next chunk with in-window entries
                 if (ovc >= 0) ovc = ov.next[ovc];
-                while (ovc < 0 && ovh < 1) { ++ovh; if (ovh >= 0) ovc = ov.head[2 * row + ovh]; }
+                while (ovc < 0 && ovh < 3) { ++ovh; if (ovh >= 0) ovc = ov.head[4 * row + ovh]; }
                 if (ovc < 0) break;
                 const int m = ov.cnt[ovc];
                 ove = lane < m ? ov.ent[(size_t)ovc * kOvfChunk + lane] : make_int2(0x7f800000, -1);
-                ovbal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(ove.x) <= ov.lim[2 * row + ovh]);
+                ovbal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(ove.x) <= ov.lim[4 * row + ovh]);
             }
             if (ovbal == 0u) break;
             const int src = __ffs(ovbal) - 1;
@@ -315,11 +344,10 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
     float4 xv[Q];
     load_row4<Q>(X, row, d4, lane, xv);
     const int cc = ccount[row];
-    const int c0 = split ? (cc & 255) : cc;
-    const int c1 = split ? ((cc >> 8) & 255) : 0;
-    int cnt = c0 + c1;
+    const CandLayout L = cand_layout(cc, split, split && ov.ngp ? (int)*ov.ngp : 2);
+    int cnt = L.cnt;
     // candidate q lives in lane q % 32, register q / 32 (up to 64 per row)
-    auto slot = [&](int q) { return q < c0 ? q : SOMB_CAND_CAP / 2 + (q - c0); };
+    auto slot = [&](int q) { return cand_slot(L, q); };
     int myj0 = lane < cnt ? cand[row * SOMB_CAND_CAP + slot(lane)] : -1;
     int myj1 = lane + 32 < cnt ? cand[row * SOMB_CAND_CAP + slot(lane + 32)] : -1;
     auto cand_at = [&](int q) {
@@ -352,10 +380,10 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
     }
     if (ov.head != nullptr && !all) {   // spilled candidates of both column groups
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            const float lim = ov.lim[2 * row + h];
+        for (int h = 0; h < 4; ++h) {
+            const float lim = ov.lim[4 * row + h];
 #pragma unroll 1
-            for (int c = ov.head[2 * row + h]; c >= 0; c = ov.next[c]) {
+            for (int c = ov.head[4 * row + h]; c >= 0; c = ov.next[c]) {
                 const int m = ov.cnt[c];
                 const int2 e = lane < m ? ov.ent[(size_t)c * kOvfChunk + lane] : make_int2(0x7f800000, -1);
                 unsigned bal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(e.x) <= lim);
@@ -430,10 +458,9 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
     float4 xv[Q];
     load_row4<Q>(X, row, d4, lane, xv);
     const int cc = ccount[row];
-    const int c0 = split ? (cc & 255) : cc;
-    const int c1 = split ? ((cc >> 8) & 255) : 0;
-    int cnt = c0 + c1;
-    auto slot = [&](int q) { return q < c0 ? q : SOMB_CAND_CAP / 2 + (q - c0); };
+    const CandLayout L = cand_layout(cc, split, split && ov.ngp ? (int)*ov.ngp : 2);
+    int cnt = L.cnt;
+    auto slot = [&](int q) { return cand_slot(L, q); };
     const int myj0 = lane < cnt ? cand[row * SOMB_CAND_CAP + slot(lane)] : -1;
     const int myj1 = lane + 32 < cnt ? cand[row * SOMB_CAND_CAP + slot(lane + 32)] : -1;
     const bool all = cnt <= 0;       // safety net: exact scan of every node
@@ -489,10 +516,10 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
     run(cnt, cand_at);
     if (ov.head != nullptr && !all) {   // spilled candidates of both column groups, chunk by chunk
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            const float lim = ov.lim[2 * row + h];
+        for (int h = 0; h < 4; ++h) {
+            const float lim = ov.lim[4 * row + h];
 #pragma unroll 1
-            for (int c = ov.head[2 * row + h]; c >= 0; c = ov.next[c]) {
+            for (int c = ov.head[4 * row + h]; c >= 0; c = ov.next[c]) {
                 const int m = ov.cnt[c];
                 const int2 e = lane < m ? ov.ent[(size_t)c * kOvfChunk + lane] : make_int2(0x7f800000, -1);
                 const unsigned bal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(e.x) <= lim);
@@ -639,8 +666,8 @@ extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int3
         g_rerank_pipe = e ? atoi(e) != 0 : 1;
     }
     int all = screen_impl == 2, split = screen_impl == 0 || screen_impl == 3;
-    OvfView ov{nullptr, nullptr, nullptr, nullptr, nullptr};
-    if (split) ov = OvfView{bw.ovf_head, bw.ovf_lim, bw.pool.ent, bw.pool.next, bw.pool.cnt};
+    OvfView ov{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (split) ov = OvfView{bw.ovf_head, bw.ovf_lim, bw.pool.ent, bw.pool.next, bw.pool.cnt, bw.ctrs + 3};
     if (all) cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
     const int wpb = 8;
     const unsigned blocks = (unsigned)((n + wpb - 1) / wpb);

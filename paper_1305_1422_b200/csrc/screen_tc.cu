@@ -51,8 +51,11 @@ constexpr int TC_ROWS = 128;                      // data rows per CTA (TMEM lan
 // D += hi.hi + hi.lo + lo.hi (~22-bit operand precision, 3x the MMAs) for
 // small feature counts where the 1-pass fp16 window holds too many
 // near-tied nodes.  A stage holds [A_hi | B_hi | A_lo | B_lo].
-template <int CG, int PASSES = 1, int HC = SOMB_CAND_CAP / 2>
+template <int CG, int PASSES = 1, int HC = SOMB_CAND_CAP / 2, int EPI = TC_EPI_WARPS>
 struct TcCfg {
+    static constexpr int EPI_WARPS = EPI;                           // 8 (2 column groups) or 16 (4 groups)
+    static constexpr int NGRP = EPI / 4;                            // column groups per row
+    static constexpr int THREADS = 32 * (2 + EPI);
     static constexpr int B_ROWS = TC_BN / CG;                      // codebook rows per CTA (smem B tile)
     static constexpr uint32_t A_BYTES = TC_ROWS * TC_BK * 2;       // 16 KB
     static constexpr uint32_t B_BYTES = B_ROWS * TC_BK * 2;        // 32 KB (CG 1) / 16 KB (CG 2)
@@ -62,7 +65,8 @@ struct TcCfg {
     // screened (value, index) pairs are kept (cand.cuh)
     static constexpr int HALF_CAP = HC;
     static_assert(HC <= SOMB_CAND_CAP / 2, "column-group capacity exceeds the candidate list");
-    static constexpr uint32_t CAND_BYTES = TC_EPI_WARPS * 32 * HALF_CAP * 8;
+    static_assert(HC * NGRP <= SOMB_CAND_CAP, "candidate slots per row exceeded");
+    static constexpr uint32_t CAND_BYTES = EPI * 32 * HALF_CAP * 8;
     static constexpr int STAGES_RAW = (224 * 1024 - CAND_BYTES) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static_assert(STAGES >= 2, "pipeline needs two stages");
@@ -264,7 +268,7 @@ __constant__ int g_a_evict_last = 0;
 // the L2 -> SM codebook traffic halves (the screen is L2-bandwidth bound).
 // Both pairs' MMAs must release a stage before it is refilled (empty
 // barriers count MC arrivals).
-template <int CG, int PASSES, int HC, int MC = 1>
+template <int CG, int PASSES, int HC, int MC = 1, int EPI = TC_EPI_WARPS>
 __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const CUtensorMap *map_w,
                                                const CUtensorMap *map_xl, const CUtensorMap *map_wl, int64_t n,
                                                int dp, int kp, const float *__restrict__ c,
@@ -274,13 +278,13 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                                                float *__restrict__ dump, unsigned *__restrict__ sync_ctr,
                                                int lag, OvfPool pool, int *__restrict__ ovf_head,
                                                float *__restrict__ ovf_lim) {
-    using Cfg = TcCfg<CG, PASSES, HC>;
+    using Cfg = TcCfg<CG, PASSES, HC, EPI>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     // stage s: A_hi at smem + s*STAGE_BYTES, B_hi after it, then A_lo, B_lo (3-pass)
     float *cbv = (float *)(smem + S * Cfg::STAGE_BYTES);
-    int *cbi = (int *)(cbv + TC_EPI_WARPS * 32 * Cfg::HALF_CAP);
+    int *cbi = (int *)(cbv + EPI * 32 * Cfg::HALF_CAP);
     uint64_t *bars = (uint64_t *)(smem + S * Cfg::STAGE_BYTES + Cfg::CAND_BYTES);
     // bars: full[S] empty[S] tfull[2] tempty[2]; then the TMEM base address
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * S + 4);
@@ -294,6 +298,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t tfull0 = smem_u32(bars + 2 * S), tempty0 = smem_u32(bars + 2 * S + 2);
 
+    if (threadIdx.x == 0 && blockIdx.x == 0) sync_ctr[3] = Cfg::NGRP;   // candidate-list layout for the re-rank
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full0 + 8 * s, 1);
@@ -301,7 +306,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull0 + 8 * a, 1);
-            mbar_init(tempty0 + 8 * a, CG * TC_EPI_WARPS);   // one arrival per epilogue warp of the pair
+            mbar_init(tempty0 + 8 * a, CG * EPI);   // one arrival per epilogue warp of the pair
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map_x)) : "memory");
@@ -466,16 +471,19 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
         }
     } else {
         // ---------------------------------------------------------- epilogue
-        // Warp group `half` takes the 32-column chunks ch = half, half+2, ...
-        // of each 256-node tile (interleaved so that a run of consecutive
-        // nodes -- neighbours on the map -- spreads over both groups).
-        const int ew = warp - 2;               // 0..7
+        // Warp group `half` (column group 0..NGRP-1) takes the 32-column
+        // chunks ch = half, half+NGRP, ... of each 256-node tile (interleaved
+        // so that a run of consecutive nodes -- neighbours on the map --
+        // spreads over the groups).  (16 epilogue warps / 4 groups were
+        // measured slower at cfg5: register spills at 576 threads.)
+        const int ew = warp - 2;               // 0..EPI-1
         const int quad = warp & 3;             // TMEM lane quadrant this warp may access
         const int half = ew >> 2;
         const int et = ew * 32 + lane;         // buffer slot owner id
+        constexpr int GS = SOMB_CAND_CAP / Cfg::NGRP;   // candidate slots per group
         const float m = scal[0];
         const float nmax = scal[1];
-        const CandBuf cb{smem_u32(cbv + et), smem_u32(cbi + et), 4u * TC_EPI_WARPS * 32};
+        const CandBuf cb{smem_u32(cbv + et), smem_u32(cbi + et), 4u * EPI * 32};
         int acc = 0;
         uint32_t aphase = 0;
         const int my_iters = MC == 1 ? (unit0 < num_units ? (num_units - unit0 + unit_step - 1) / unit_step : 0) : iters;
@@ -501,7 +509,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                 }
                 const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN);
 #pragma unroll 1
-                for (int ch = half; ch < TC_BN / 32; ch += 2) {
+                for (int ch = half; ch < TC_BN / 32; ch += Cfg::NGRP) {
                     float v[32];
                     tmem_ld32(tbase + ch * 32, v);
                     const int jc = nt * TC_BN + ch * 32;
@@ -543,13 +551,14 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
             if (live) {
-                int *out = cand + row * SOMB_CAND_CAP + half * (SOMB_CAND_CAP / 2);
+                int *out = cand + row * SOMB_CAND_CAP + half * GS;
                 int cnt = cand_emit<Cfg::HALF_CAP>(st, cb, out);
-                // two column groups write disjoint bytes of ccount / flags
+                // the column groups write disjoint bytes of ccount / flags
                 reinterpret_cast<uint8_t *>(ccount + row)[half] = (uint8_t)cnt;
                 reinterpret_cast<uint8_t *>(flags + row)[half] = (uint8_t)st.trunc;
-                ovf_head[2 * row + half] = st.head;
-                ovf_lim[2 * row + half] = st.rmin + st.win;
+                ovf_head[4 * row + half] = st.head;
+                ovf_lim[4 * row + half] = st.rmin + st.win;
+                if (Cfg::NGRP == 2) ovf_head[4 * row + 2 + half] = -1;
             }
         }
     }
@@ -751,7 +760,8 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
                                                                      ovf_head, ovf_lim)
     if (two) {
         SOMB_REQUIRE(cg == 2, SOMB_E_CONFIG, "screen_tc: the fp8 split screen needs CTA pairs (tc_group 2)");
-        if (mcv == 2) SCREEN_LAUNCH(screen_tc4_kernel, 2, 2, 32); else SCREEN_LAUNCH(screen_tc2_kernel, 2, 2, 32);
+        if (mcv == 2) SCREEN_LAUNCH(screen_tc4_kernel, 2, 2, 32);
+        else SCREEN_LAUNCH(screen_tc2_kernel, 2, 2, 32);
     } else if (cg == 1) {
         if (three) SCREEN_LAUNCH(screen_tc1_kernel, 1, 3, 16); else SCREEN_LAUNCH(screen_tc1_kernel, 1, 1, 16);
     } else if (mcv == 2) {

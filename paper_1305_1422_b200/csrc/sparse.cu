@@ -121,9 +121,8 @@ sp_screen_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col
     if (lane == 0) {
         ccount[row] = cand_emit<SP_CAP>(st, cb, cand + row * SOMB_CAND_CAP);
         flags[row] = st.trunc;
-        ovf_head[2 * row] = st.head;          // one column group: slot 1 stays empty
-        ovf_head[2 * row + 1] = -1;
-        ovf_lim[2 * row] = st.rmin + st.win;
+        ovf_head[4 * row] = st.head;          // one column group: slots 1..3 stay empty
+        ovf_lim[4 * row] = st.rmin + st.win;
     }
 }
 
@@ -246,9 +245,8 @@ sp_screen_ls_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ 
             const CandBufG cb{gbv + row * SP_CAP, gbi + row * SP_CAP};
             ccount[row] = cand_emit<SP_CAP>(st, cb, cand + row * SOMB_CAND_CAP);
             flags[row] = st.trunc;
-            ovf_head[2 * row] = st.head;
-            ovf_head[2 * row + 1] = -1;
-            ovf_lim[2 * row] = st.rmin + st.win;
+            ovf_head[4 * row] = st.head;
+            ovf_lim[4 * row] = st.rmin + st.win;
         }
     }
 }
@@ -285,8 +283,8 @@ __global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *
     };
     for (int q = 0; q < cnt; ++q) eval(scan ? q : cand[row * SOMB_CAND_CAP + q]);
     if (!scan) {   // spilled candidates (the screen's overflow chunks within the final window)
-        const float lim = ovf_lim[2 * row];
-        for (int c = ovf_head[2 * row]; c >= 0; c = pool.next[c]) {
+        const float lim = ovf_lim[4 * row];
+        for (int c = ovf_head[4 * row]; c >= 0; c = pool.next[c]) {
             const int m = pool.cnt[c];
             const int2 e = lane < m ? pool.ent[(size_t)c * kOvfChunk + lane] : make_int2(0x7f800000, -1);
             unsigned bal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(e.x) <= lim);

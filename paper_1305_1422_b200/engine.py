@@ -345,8 +345,8 @@ class SomEngine:
         """Per-row candidate counts of the last screen (tcgen05 two-half encoding)."""
         off = ((self.n * _lib.CAND_CAP * 4 + 255) // 256) * 256
         cc = self.ws[off: off + 4 * self.n].view(torch.int32)
-        if self.screen_impl in (0, 3):
-            return (cc & 255) + ((cc >> 8) & 255)
+        if self.screen_impl in (0, 3):   # one count byte per column group (2 or 4 groups)
+            return (cc & 255) + ((cc >> 8) & 255) + ((cc >> 16) & 255) + ((cc >> 24) & 255)
         return cc
 
     def overflow_chunks(self) -> int:

@@ -34,8 +34,8 @@ for e in range(10):
     torch.cuda.synchronize()
     cc = eng.candidate_counts()[: eng.n].float().cpu().numpy()
     fl = eng.flags[: eng.n].cpu().numpy()
-    trunc = float((((fl & 0xFF) | ((fl >> 8) & 0xFF)) & 1).astype(bool).mean())
-    spilled = float((((fl & 0xFF) | ((fl >> 8) & 0xFF)) & 2).astype(bool).mean())
+    trunc = float((((fl & 0xFF) | ((fl >> 8) & 0xFF) | ((fl >> 16) & 0xFF) | ((fl >> 24) & 0xFF)) & 1).astype(bool).mean())
+    spilled = float((((fl & 0xFF) | ((fl >> 8) & 0xFF) | ((fl >> 16) & 0xFF) | ((fl >> 24) & 0xFF)) & 2).astype(bool).mean())
     chunks = eng.overflow_chunks() if eng.screen_impl == 0 and eng.passes >= 1 else 0
     eng._mark("node_sums", True)
     eng.qe_sum()

@@ -24,7 +24,7 @@ for e in range(E):
     eng.search()
     cc = eng.candidate_counts()[:n].float().cpu().numpy()
     fl = eng.flags[:n].cpu().numpy()
-    tr = (((fl & 0xFF) | ((fl >> 8) & 0xFF)) & 1).astype(bool)
+    tr = (((fl & 0xFF) | ((fl >> 8) & 0xFF) | ((fl >> 16) & 0xFF) | ((fl >> 24) & 0xFF)) & 1).astype(bool)
     bm = eng.bmu[:m].cpu().numpy().copy()
     ref.set_codebook(eng.codebook())
     ref.search()
