@@ -166,7 +166,24 @@ seg_sum(const float *__restrict__ X, int d, const int *__restrict__ perm, const 
         double acc[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) acc[q] = 0.0;
-        for (int r = r0; r < r1; ++r) {
+        // rows in fixed ascending order; four rows' loads in flight at a time
+        int r = r0;
+        for (; r + 4 <= r1; r += 4) {
+            const float *x0 = X + (int64_t)perm[r] * d, *x1 = X + (int64_t)perm[r + 1] * d;
+            const float *x2 = X + (int64_t)perm[r + 2] * d, *x3 = X + (int64_t)perm[r + 3] * d;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                int k = k0 + q * 128 + threadIdx.x;
+                if (k < d) {
+                    const float a = __ldg(x0 + k), b = __ldg(x1 + k), cc = __ldg(x2 + k), e = __ldg(x3 + k);
+                    acc[q] += (double)a;
+                    acc[q] += (double)b;
+                    acc[q] += (double)cc;
+                    acc[q] += (double)e;
+                }
+            }
+        }
+        for (; r < r1; ++r) {
             const float *x = X + (int64_t)perm[r] * d;
 #pragma unroll
             for (int q = 0; q < R; ++q) {
