@@ -386,3 +386,41 @@ def test_device_codebook_init_bit_exact(seed, nx, ny, d):
     eng.init_codebook_device(seed)
     ref = np.random.default_rng(seed).random((nx * ny, d), dtype=np.float32)
     np.testing.assert_array_equal(eng.codebook(), ref)
+
+
+@pytest.mark.parametrize("screen", ["tensor", "exact"])
+@pytest.mark.parametrize("n,d,nx,ny,mt", [(1, 3, 2, 2, "planar"), (5, 1, 1, 1, "toroid"), (130, 7, 3, 5, "toroid"),
+                                          (257, 300, 17, 1, "planar"), (300, 1024, 16, 16, "toroid"),
+                                          (200, 2000, 8, 8, "planar")])
+def test_edge_shapes_train_vs_oracle(screen, n, d, nx, ny, mt):
+    """Odd shapes: a single row, a 1x1 map, d = 1, one-row maps, partial
+    128-row units, the widest supported re-rank row (d = 1024)."""
+    rng = np.random.default_rng(n * 31 + d)
+    x = rng.random((n, d), dtype=np.float32)
+    cfg = S.TrainConfig(n_epochs=3, n_columns=nx, n_rows=ny, map_type=S.MapType(mt), kernel=S.Kernel.DENSE_BLOCKED)
+    cb, bmus, u = S.train(S.DenseDataset(x), cfg, options=_opts(screen))
+    w, bm, uo, _ = O.train(x, nx, ny, n_epochs=3, map_type=O.TOROID if mt == "toroid" else O.PLANAR)
+    rel = np.max(np.abs(cb.weights.astype(np.float64) - w) / np.maximum(np.abs(w), 1e-12))
+    assert rel <= 1e-4, rel
+    assert np.mean(np.any(bmus != bm, axis=1)) <= 1e-2
+
+
+@pytest.mark.parametrize("screen", ["tensor", "exact"])
+def test_sparse_empty_rows_vs_oracle(screen):
+    """CSR rows without nonzeros (they still count in the denominators,
+    kernels.py:233-237) mixed with ordinary rows, sparse train vs the oracle."""
+    rng = np.random.default_rng(77)
+    n, d = 400, 300
+    nnz = rng.integers(0, 12, n)
+    nnz[::7] = 0
+    offsets = np.concatenate([[0], np.cumsum(nnz)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(d, k, replace=False)) for k in nnz]).astype(np.int32)
+    vals = rng.random(int(offsets[-1]), dtype=np.float32)
+    data = S.SparseDataset(d, offsets, cols, vals)
+    init = rng.random((6 * 5, d), dtype=np.float32)
+    cfg = S.TrainConfig(n_epochs=4, n_columns=6, n_rows=5, kernel=S.Kernel.SPARSE)
+    cb, bmus, u = S.train(data, cfg, initial_codebook=S.CodeBook(6, 5, d, init), options=_opts(screen))
+    w, bm, uo, _ = O.train(O.CSR(d, offsets, cols, vals), 6, 5, n_epochs=4, kernel=O.SPARSE, initial_codebook=init)
+    rel = np.max(np.abs(cb.weights.astype(np.float64) - w) / np.maximum(np.abs(w), 1e-12))
+    assert rel <= 1e-4, rel
+    assert np.mean(np.any(bmus != bm, axis=1)) <= 1e-2
