@@ -258,6 +258,15 @@ SOMB_API int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col,
 /* Number of kernels this library has launched (process lifetime). */
 SOMB_API unsigned long long somb_launch_count(void);
 
+/* ---- artifact text (fileio.py:322-359), host code, no GPU needed --------
+ * The reference's Python formatting f"{float(v):.6g}", space-separated,
+ * one row per line; BMU lines "i row col".  Formats into `out` (capacity
+ * `cap` bytes) on `threads` host threads and returns the byte count, or
+ * -(bytes needed) if `cap` is too small. */
+SOMB_API int64_t somb_format_f32_rows(const float *v, int64_t rows, int64_t cols, char *out, int64_t cap,
+                                      int32_t threads);
+SOMB_API int64_t somb_format_bmus(const int32_t *bm, int64_t n, char *out, int64_t cap, int32_t threads);
+
 /* ---- U-matrix (umatrix.py:26-45; hex adjacency = extension) ---------- */
 SOMB_API int somb_umatrix(const float *W, int32_t d, const somb_map *map, float *U,
                  void *stream);

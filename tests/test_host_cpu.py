@@ -190,3 +190,23 @@ def test_device_init_restatement_matches_numpy(seed):
     ref = np.random.default_rng(seed).random(5000, dtype=np.float32)
     for start, count in [(0, 17), (1, 9), (2048, 33), (4095, 7), (4990, 10)]:
         np.testing.assert_array_equal(_pcg64_floats(seed, start, count), ref[start:start + count])
+
+
+def test_native_writers_match_reference_format(tmp_path):
+    """somb_format_* == the reference's f"{float(v):.6g}" lines
+    (fileio.py:322-359), including -0, inf, nan, subnormal-range and
+    exponent-boundary values."""
+    from paper_1305_1422_b200 import fileio
+    rng = np.random.default_rng(11)
+    w = (rng.standard_normal((300, 13)) * 10.0 ** rng.integers(-38, 38, (300, 13))).astype(np.float32)
+    w[0, :8] = [0.0, -0.0, np.inf, -np.inf, np.nan, 1e-5, 123456.5, 1e6]
+    w[1, :5] = [0.1, -3.5e-38, 1e-45, 999999.5, 0.000123456789]
+    cb = S.CodeBook(15, 20, 13, w)
+    fileio.write_codebook(cb, str(tmp_path / "a.wts"))
+    ref = f"% {cb.n_rows} {cb.n_columns}\n% {cb.n_dimensions}\n" + "".join(
+        " ".join(f"{float(v):.6g}" for v in node) + "\n" for node in w)
+    assert (tmp_path / "a.wts").read_bytes() == ref.encode()
+    bm = rng.integers(0, 300, (5000, 2)).astype(np.int32)
+    fileio.write_bmus(bm, str(tmp_path / "a.bm"))
+    ref = f"% {len(bm)}\n" + "".join(f"{i} {r} {c}\n" for i, (r, c) in enumerate(bm))
+    assert (tmp_path / "a.bm").read_bytes() == ref.encode()
