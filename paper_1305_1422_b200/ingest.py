@@ -1,0 +1,178 @@
+"""Dataset text ingest with the reference formats (fileio.py:1-317): plain
+dense, '%'-headered dense and zero-based sparse ``index:value`` rows,
+content-detected; '#' comments, LF or CRLF.  Values become float32 exactly
+as numpy converts the tokens (the reference's np.array(tokens, float32)).
+Rows are converted in bulk (one numpy conversion per file, not per row);
+the per-line error checks and messages follow the reference's."""
+from __future__ import annotations
+
+import numpy as np
+
+from . import errors
+from .datasets import DenseDataset, SparseDataset
+
+
+def _lines(src) -> list:
+    if isinstance(src, bytes):
+        src = src.decode("utf-8")
+    if not isinstance(src, str):
+        src = src.read()
+    return src.splitlines()
+
+
+def _comment(line: str) -> bool:
+    return line.lstrip().startswith("#")
+
+
+def _is_number(tok: str) -> bool:
+    try:
+        float(tok)
+        return True
+    except ValueError:
+        return False
+
+
+def _to_f32(tokens: list, lineno_of) -> np.ndarray:
+    """Bulk conversion; on failure locate the first bad token for the
+    reference's NonNumericToken message (line-accurate)."""
+    try:
+        vals = np.array(tokens, dtype=np.float32)
+    except ValueError:
+        for k, t in enumerate(tokens):
+            if not _is_number(t):
+                raise errors.NonNumericToken(f"line {lineno_of(k)}: token {t!r} is not a number") from None
+        raise
+    bad = np.flatnonzero(~np.isfinite(vals))
+    if bad.size:
+        raise errors.NonNumericToken(f"line {lineno_of(int(bad[0]))}: non-finite value")
+    return vals
+
+
+def _dense_body(rows: list, width: int, mismatch) -> DenseDataset:
+    """rows: [(lineno, tokens)] all of `width` tokens (checked here)."""
+    for lineno, toks in rows:
+        if len(toks) != width:
+            raise mismatch(f"line {lineno}: expected {width} values, got {len(toks)}")
+    flat = [t for _, toks in rows for t in toks]
+    linenos = [no for no, _ in rows]
+    vals = _to_f32(flat, lambda k: linenos[k // max(width, 1)])
+    return DenseDataset(vals.reshape(len(rows), width))
+
+
+def parse_dense(src) -> DenseDataset:
+    """Plain dense text (fileio.py:150-165)."""
+    rows = [(no, ln.split()) for no, ln in enumerate(_lines(src), 1) if ln.strip() and not _comment(ln)]
+    if not rows:
+        raise errors.EmptyInput("no data rows found")
+    return _dense_body(rows, len(rows[0][1]), errors.RowWidthMismatch)
+
+
+def _header_counts(line: str, lineno: int) -> list:
+    counts = []
+    for tok in line.lstrip()[1:].split():   # "%2" and "% 2" both; trailing words ignored
+        try:
+            counts.append(int(tok))
+        except ValueError:
+            break
+    if not counts:
+        raise errors.MalformedHeader(f"line {lineno}: no count in header {line!r}")
+    if min(counts) < 0:
+        raise errors.MalformedHeader(f"line {lineno}: negative count in header")
+    return counts
+
+
+def parse_dense_headered(src) -> DenseDataset:
+    """Dense text after two '%' count headers: instances (a two-number header
+    is a grid whose product is the count), then dimensions (fileio.py:186-229)."""
+    headers, rows = [], []
+    for no, ln in enumerate(_lines(src), 1):
+        s = ln.strip()
+        if not s or _comment(ln):
+            continue
+        if s.startswith("%"):
+            if len(headers) == 2:
+                raise errors.MalformedHeader(f"line {no}: unexpected extra header")
+            headers.append(_header_counts(ln, no))
+        elif len(headers) < 2:
+            raise errors.MalformedHeader(f"line {no}: data before both header lines")
+        else:
+            rows.append((no, s.split()))
+    if len(headers) < 2:
+        raise errors.MalformedHeader("missing '%' header lines")
+    n = headers[0][0] * headers[0][1] if len(headers[0]) >= 2 else headers[0][0]
+    d = headers[1][0]
+    if len(rows) != n:
+        raise errors.HeaderBodyMismatch(f"header declares {n} rows, body has {len(rows)}")
+    if n == 0:
+        return DenseDataset(np.empty((0, d), dtype=np.float32))
+    return _dense_body(rows, d, errors.HeaderBodyMismatch)
+
+
+def parse_sparse(src, n_dimensions_hint=None) -> SparseDataset:
+    """Zero-based ``index:value`` rows into CSR, indices sorted per row, a
+    duplicate index an error, an empty line an all-zero instance, an empty
+    file one all-zero instance (fileio.py:232-283)."""
+    lines = _lines(src) or [""]
+    offsets, cols, vals = [0], [], []
+    top = -1
+    for no, ln in enumerate(lines, 1):
+        if _comment(ln):
+            continue
+        row = []
+        for tok in ln.split():
+            i_s, sep, v_s = tok.partition(":")
+            if not sep:
+                raise errors.MalformedToken(f"line {no}: token {tok!r} is not index:value")
+            try:
+                idx = int(i_s)
+            except ValueError:
+                raise errors.MalformedToken(f"line {no}: bad index in token {tok!r}") from None
+            if idx < 0:
+                raise errors.NegativeIndex(f"line {no}: index {idx} is negative")
+            if not _is_number(v_s):
+                raise errors.MalformedToken(f"line {no}: bad value in token {tok!r}")
+            v = float(v_s)
+            if not np.isfinite(np.float32(v)):
+                raise errors.MalformedToken(f"line {no}: non-finite value")
+            row.append((idx, v))
+        row.sort(key=lambda e: e[0])
+        for a, b in zip(row, row[1:]):
+            if a[0] == b[0]:
+                raise errors.DuplicateIndexInRow(f"line {no}: index {a[0]} appears twice")
+        if row:
+            top = max(top, row[-1][0])
+        cols += [e[0] for e in row]
+        vals += [e[1] for e in row]
+        offsets.append(len(cols))
+    d = top + 1
+    if n_dimensions_hint is not None:
+        if n_dimensions_hint < d:
+            raise errors.HintTooSmall(f"dimension hint {n_dimensions_hint} < required {d}")
+        d = n_dimensions_hint
+    return SparseDataset(d, np.array(offsets, dtype=np.int64), np.array(cols, dtype=np.int32),
+                         np.array(vals, dtype=np.float32))
+
+
+def detect_format(lines) -> str:
+    """'headered' if the first data line starts with '%', 'sparse' if its
+    first token holds ':', else 'dense' (fileio.py:286-302)."""
+    for ln in lines:
+        s = ln.strip()
+        if not s or _comment(ln):
+            continue
+        if s.startswith("%"):
+            return "headered"
+        return "sparse" if ":" in s.split()[0] else "dense"
+    return "dense"
+
+
+def read_dataset(path: str):
+    """(dataset, format) from a file, format auto-detected (fileio.py:305-317)."""
+    try:
+        with open(path, "r", encoding="utf-8") as fh:
+            text = fh.read()
+    except OSError as exc:
+        raise errors.IoFailure(f"cannot read {path}: {exc}") from exc
+    fmt = detect_format(text.splitlines())
+    parse = {"sparse": parse_sparse, "headered": parse_dense_headered, "dense": parse_dense}[fmt]
+    return parse(text), fmt

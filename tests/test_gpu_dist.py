@@ -74,3 +74,38 @@ def test_sharded_train_sparse_two_ranks_one_gpu(tmp_path):
     import oracle as O
     sp = O.gen_random_sparse(3000, 400, 0.02, 11)
     _run(tmp_path, (sp.n_dimensions, sp.row_offsets, sp.col_indices, sp.values), sparse=True)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+def test_cli_local_and_torchrun_two_ranks(tmp_path):
+    """The CLI (reference flags) trains and writes .wts/.bm/.umx (+ -s 2
+    snapshots); under torchrun with two ranks on one GPU (gloo) rank 0 writes
+    artifacts matching the single-process run."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    import paper_1305_1422_b200 as S
+    from paper_1305_1422_b200 import fileio
+    rng = np.random.default_rng(3)
+    x = rng.random((3000, 12), dtype=np.float32)
+    inp = tmp_path / "data.txt"
+    inp.write_text("".join(" ".join(f"{v:.6g}" for v in row) + "\n" for row in x))
+    args = ["-x", "9", "-y", "7", "-m", "toroid", "-k", "1", "-e", "4", "-s", "2", str(inp)]
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    one = subprocess.run([sys.executable, "-m", "paper_1305_1422_b200"] + args + [str(tmp_path / "one")],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert one.returncode == 0, one.stderr[-2000:]
+    assert one.stdout.count("epoch ") == 4
+    for ext in ("wts", "bm", "umx"):
+        assert (tmp_path / f"one.{ext}").exists() and (tmp_path / f"one.3.{ext}").exists()
+    env2 = dict(env, SOMB_DIST_BACKEND="gloo")
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "-m",
+                          "paper_1305_1422_b200"] + args + [str(tmp_path / "two")],
+                         capture_output=True, text=True, timeout=600, env=env2, cwd=ROOT)
+    assert two.returncode == 0, two.stderr[-3000:]
+    n1, m1, w1 = fileio.load_codebook(str(tmp_path / "one.wts"))
+    n2, m2, w2 = fileio.load_codebook(str(tmp_path / "two.wts"))
+    assert (n1, m1) == (n2, m2) == (9, 7)
+    assert np.max(np.abs(w1.astype(np.float64) - w2) / np.maximum(np.abs(w1), 1e-6)) <= 1e-4
+    assert (tmp_path / "two.bm").read_text().count("\n") == 3001
