@@ -266,6 +266,15 @@ SOMB_API unsigned long long somb_launch_count(void);
 SOMB_API int64_t somb_format_f32_rows(const float *v, int64_t rows, int64_t cols, char *out, int64_t cap,
                                       int32_t threads);
 SOMB_API int64_t somb_format_bmus(const int32_t *bm, int64_t n, char *out, int64_t cap, int32_t threads);
+/* Dense text ingest (fileio.py:150-229), host code: scan (data rows, columns
+ * of the first data row, '%' header lines, first width-mismatch line), then
+ * parse into row-major f32 on `threads` threads (tokens as double, rounded
+ * to f32).  The parse returns 0 or the line number of the first row needing
+ * the reference-exact error path. */
+SOMB_API int64_t somb_scan_dense_text(const char *buf, int64_t len, int64_t *cols, int64_t *n_headers,
+                                      int64_t *bad_line);
+SOMB_API int64_t somb_parse_dense_text(const char *buf, int64_t len, int64_t rows, int64_t cols, float *out,
+                                       int32_t threads);
 
 /* ---- U-matrix (umatrix.py:26-45; hex adjacency = extension) ---------- */
 SOMB_API int somb_umatrix(const float *W, int32_t d, const somb_map *map, float *U,

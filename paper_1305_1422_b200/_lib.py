@@ -64,6 +64,8 @@ SIGNATURES = {
     "somb_launch_count": (C.c_ulonglong, []),
     "somb_format_f32_rows": (I64, [P, I64, I64, P, I64, I32]),
     "somb_format_bmus": (I64, [P, I64, P, I64, I32]),
+    "somb_scan_dense_text": (I64, [P, I64, P, P, P]),
+    "somb_parse_dense_text": (I64, [P, I64, I64, I64, P, I32]),
     "somb_uniform_f32": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, I64, P, P]),
     "somb_set_knob": (C.c_int, [C.c_char_p, I32]),
     "somb_node_sums_ws": (SZ, [I64, I32, I32]),

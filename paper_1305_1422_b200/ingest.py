@@ -166,13 +166,66 @@ def detect_format(lines) -> str:
     return "dense"
 
 
-def read_dataset(path: str):
-    """(dataset, format) from a file, format auto-detected (fileio.py:305-317)."""
+def _native_dense(raw: bytes, fmt: str):
+    """Dense / headered body through the library's threaded parser
+    (somb_scan_dense_text / somb_parse_dense_text); None when the input needs
+    the reference-exact Python path (errors, unusual tokens, header layout)."""
+    import ctypes as C
+    import os
+    from . import _lib
     try:
-        with open(path, "r", encoding="utf-8") as fh:
-            text = fh.read()
+        lib = _lib.load()
+    except errors.DeviceError:
+        return None
+    cols, nh, bad = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+    rows = lib.somb_scan_dense_text(raw, len(raw), C.byref(cols), C.byref(nh), C.byref(bad))
+    if bad.value or rows == 0:
+        return None
+    if fmt == "headered":
+        if nh.value != 2:
+            return None
+        head, seen = [], 0
+        for no, ln in enumerate(raw.decode("utf-8", errors="replace").splitlines(), 1):
+            t = ln.strip()
+            if not t or _comment(ln):
+                continue
+            if not t.startswith("%"):
+                break                        # data before the second header: Python path raises
+            head.append(_header_counts(ln, no))
+            seen += 1
+            if seen == 2:
+                break
+        if len(head) < 2:
+            return None
+        n = head[0][0] * head[0][1] if len(head[0]) >= 2 else head[0][0]
+        if n != rows or head[1][0] != cols.value:
+            return None
+    elif nh.value:
+        return None
+    out = np.empty((rows, cols.value), dtype=np.float32)
+    rc = lib.somb_parse_dense_text(raw, len(raw), rows, cols.value, out.ctypes.data_as(C.c_void_p),
+                                   min(32, os.cpu_count() or 1))
+    return DenseDataset(out) if rc == 0 else None
+
+
+def read_dataset(path: str):
+    """(dataset, format) from a file, format auto-detected (fileio.py:305-317).
+    Dense bodies go through the native parser; errors and edge cases through
+    the reference-exact Python parsers."""
+    try:
+        with open(path, "rb") as fh:
+            raw = fh.read()
     except OSError as exc:
         raise errors.IoFailure(f"cannot read {path}: {exc}") from exc
-    fmt = detect_format(text.splitlines())
+    try:
+        head = raw[:1 << 16].decode("utf-8", errors="ignore").splitlines()
+        fmt = detect_format(head if len(raw) > (1 << 16) else raw.decode("utf-8").splitlines())
+    except UnicodeDecodeError as exc:
+        raise errors.IoFailure(f"cannot read {path}: {exc}") from exc
+    if fmt in ("dense", "headered"):
+        ds = _native_dense(raw, fmt)
+        if ds is not None:
+            return ds, fmt
+    text = raw.decode("utf-8")
     parse = {"sparse": parse_sparse, "headered": parse_dense_headered, "dense": parse_dense}[fmt]
     return parse(text), fmt

@@ -72,3 +72,32 @@ def test_module_entry_point_help():
     out = subprocess.run([sys.executable, "-m", "paper_1305_1422_b200", "--help"], capture_output=True, text=True,
                          cwd=ROOT, timeout=120)
     assert out.returncode == 0 and "INPUT_FILE" in out.stdout and "--compact-support" in out.stdout
+
+
+def test_native_dense_ingest_matches_python_path(tmp_path):
+    """read_dataset's threaded native parser gives the values of the
+    reference-exact path (np.array(tokens, float32)), with '+' signs, CRLF,
+    comments and blank lines; error inputs fall back to the same exceptions."""
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal((3000, 17)) * 10.0 ** rng.integers(-5, 5, (3000, 17))).astype(np.float32)
+    lines = []
+    for i, row in enumerate(x):
+        toks = [("+" if (v > 0 and (i + j) % 7 == 0) else "") + repr(float(v)) for j, v in enumerate(row)]
+        lines.append(" ".join(toks) + ("\r\n" if i % 5 == 0 else "\n"))
+    text = "# header comment\n\n" + "".join(lines)
+    p = tmp_path / "x.txt"
+    p.write_text(text)
+    ds, fmt = ingest.read_dataset(str(p))
+    assert fmt == "dense"
+    np.testing.assert_array_equal(ds.values, ingest.parse_dense(text).values)
+    q = tmp_path / "h.txt"
+    q.write_text(f"% {len(x)}\n% 17\n" + "".join(lines))
+    ds2, fmt2 = ingest.read_dataset(str(q))
+    assert fmt2 == "headered"
+    np.testing.assert_array_equal(ds2.values, ds.values)
+    for bad, exc in [("1 2\n+-3 4\n", errors.NonNumericToken), ("1 2\n3 inf\n", errors.NonNumericToken),
+                     ("1 2\n3\n", errors.RowWidthMismatch), ("% 2\n1 2\n% 2\n3 4\n", errors.MalformedHeader)]:
+        b = tmp_path / "b.txt"
+        b.write_text(bad)
+        with pytest.raises(exc):
+            ingest.read_dataset(str(b))
