@@ -45,6 +45,7 @@ CONFIGS = {
 METRIC = "epoch time & BMU dist-evals/s (N·K·D) at 1/2/4/8 B200, % of roofline"
 UNIT = "dist-evals/s"
 N_EPOCHS = 10
+L2_FLUSH_BYTES = 256 << 20   # > the 126 MB L2
 
 
 def peaks():
@@ -88,6 +89,15 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
+        post = False
+        if not out.strip():   # region shorter than one sampling period: one query right after it
+            post = True
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=10).stdout
+            except (OSError, subprocess.SubprocessError):
+                out = ""
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
@@ -103,7 +113,8 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                **({"sampled": "once, right after a timed region shorter than 200 ms"} if post else {})}
 
 
 def init_dist(args):
@@ -253,16 +264,31 @@ def run_ours(args):
     t_end = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier()
-    t_start.record()
-    for s in range(args.warmup, args.warmup + args.steps):
-        r, sc = schedule_for(args.config, s)
-        eng.epoch(r, sc, 1e-3, nb, compact)
-    t_end.record()
-    torch.cuda.synchronize()
+    in_bytes = count * SPARSE_NNZ * 8 if sparse else count * d * 4
+    flush = in_bytes < L2_FLUSH_BYTES
+    if not flush:   # inputs larger than L2: one event pair around all K steps
+        t_start.record()
+        for s in range(args.warmup, args.warmup + args.steps):
+            r, sc = schedule_for(args.config, s)
+            eng.epoch(r, sc, 1e-3, nb, compact)
+        t_end.record()
+        torch.cuda.synchronize()
+        elapsed = t_start.elapsed_time(t_end) / 1e3
+    else:           # inputs fit in L2: write a larger-than-L2 buffer between timed steps
+        scratch = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for i, s in enumerate(range(args.warmup, args.warmup + args.steps)):
+            scratch.fill_(float(i))
+            r, sc = schedule_for(args.config, s)
+            ev[i][0].record()
+            eng.epoch(r, sc, 1e-3, nb, compact)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        elapsed = sum(a.elapsed_time(b) for a, b in ev) / 1e3
     barrier()
     launches = lib.somb_launch_count() - l0
     clk = clocks.stop()
-    elapsed = t_start.elapsed_time(t_end) / 1e3
     phase_ms = {k: [a.elapsed_time(b) for a, b in v] for k, v in eng.timing.items()}
     eng.timing = None
     tmax = torch.tensor([elapsed], dtype=torch.float64, device=dev)
@@ -291,7 +317,11 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": "screen_tc2_kernel (tcgen05 cta_group::2 kind::f16)",
+    passes = getattr(eng, "passes", 1)
+    kname = {1: "screen_tc4_kernel (tcgen05 cta_group::2 kind::f16, 4-CTA clusters multicasting codebook tiles)",
+             2: "screen_tc2_kernel (tcgen05 cta_group::2, fp16 kind::f16 + fp8 kind::f8f6f4 split screen)",
+             3: "screen_tc2_kernel (tcgen05 cta_group::2 kind::f16, three-pass split screen)"}.get(passes, "screen_tc")
+    roofline = {"bound": "tensor", "kernel": kname,
                 "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
                 "peak_kind": f"{pk_kind} bf16 dense sustained (fp16 kind::f16 runs at the bf16 rate)",
                 "frac_of_burst": achieved / pk.get("bf16_tflops", peak_sus),
@@ -305,7 +335,7 @@ def run_ours(args):
     if sparse:
         simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12
         gflops = 2.0 * count * SPARSE_NNZ * K / (scr_ms / 1e3) / 1e12
-        roofline = {"bound": "hbm", "kernel": "sp_screen_kernel (fp32 gather over the transposed codebook)",
+        roofline = {"bound": "hbm", "kernel": "sp_screen_ls_kernel (fp32 slab-lockstep gather over the transposed codebook)",
                     "achieved": achieved_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved_gbs / pk["hbm_gbs"], "traffic": traffic,
                     "bytes_per_launch": unique, "avg_launch_ms": scr_ms,
@@ -372,7 +402,9 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None,
-                "dtype": "fp16 tensor-core screen (fp32 accumulate) + f64 exact re-rank/update",
+                "dtype": ("fp32 gather screen + f64 exact re-rank/update" if sparse else
+                          {1: "fp16", 2: "fp16 + fp8 split", 3: "fp16 three-pass split"}.get(passes, "fp16")
+                          + " tensor-core screen (fp32 accumulate) + f64 exact re-rank/update"),
                 "data": "synthetic uniform [0,1) fp32 (torch.Generator seed 1001+rank), codebook "
                         "init default_rng(1)",
                 "config": {"workload": desc, "rows": n, "K": K, "d": d,
@@ -380,7 +412,9 @@ def run_ours(args):
                                        f"scale 1->0.01; step s = epoch s mod {N_EPOCHS}",
                            "parallelism": f"dp{world} (rows sharded, 1 fp64 all-reduce + 1 fp32 "
                                           f"all-gather per epoch)",
-                           "l2": "inputs larger than L2 (X 4 GB + fp16 copy 2 GB per GPU at cfg2)",
+                           "l2": (f"L2 flushed between timed steps (inputs {in_bytes / 1e6:.0f} MB per GPU, "
+                                  f"{L2_FLUSH_BYTES >> 20} MiB buffer written)") if flush else
+                                 f"inputs larger than L2 ({in_bytes / 1e9:.2f} GB per GPU)",
                            "screen": args.screen},
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
                 "gpu_launches": int(launches),
