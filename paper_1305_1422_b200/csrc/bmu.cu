@@ -416,7 +416,8 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
 // instead of one -- the plain kernel was bound by memory-level parallelism
 // (profiles/).  A lane only ever reads back what it copied itself, so
 // cp.async.wait_group alone orders the data (no warp barrier).  Same
-// arithmetic and order as rerank_vec_kernel.
+// products as rerank_vec_kernel (exact in fp64); eight accumulators instead
+// of four (the DFMA dependency chains were the top stall).
 constexpr int RS = 4;            // candidate rows in flight per warp
 constexpr int RP_WARPS = 4;      // warps per block
 
@@ -426,6 +427,72 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// fp32 -> fp64 without the XU pipe: the fp32 bit pattern re-read as an fp64
+// with the same exponent field is exactly w * 2^-896 (normal, subnormal and
+// zero alike); the 2^896 goes into the other operand, so every product and
+// difference below is bit-identical to the (double)w form.  3 ALU ops + 1
+// shift instead of one F2F.F64.F32, which issues at 1/8 warp-rate (it was the
+// busiest pipe of the re-rank; profiles/).  Inf / NaN codebook entries are not
+// preserved (they are finite garbage here, as anywhere after such an update).
+__device__ __forceinline__ double f32_as_f64_scaled(float v) {
+    const unsigned u = __float_as_uint(v);
+    return __hiloint2double((int)(((u & 0x7FFFFFFFu) >> 3) | (u & 0x80000000u)), (int)(u << 29));
+}
+constexpr double kF64Scale = 0x1p896;
+
+// Row operand of the pipelined re-rank: slices q < PQA convert w with F2F,
+// the rest with f32_as_f64_scaled (blocked mode keeps those x slices
+// pre-scaled by 2^896, exact since |x| < 2^128), splitting the conversions
+// over the XU and integer pipes.
+template <int Q>
+struct PipeSplit { static constexpr int PQA = (3 * Q) / 8; };
+
+template <int Q, int MODE>
+__device__ __forceinline__ void row_operand(const float4 (&x)[Q], double (&xd)[Q][4]) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const double sc = (MODE != SOMB_DIST_NAIVE && q >= PipeSplit<Q>::PQA) ? kF64Scale : 1.0;
+        xd[q][0] = (double)x[q].x * sc; xd[q][1] = (double)x[q].y * sc;
+        xd[q][2] = (double)x[q].z * sc; xd[q][3] = (double)x[q].w * sc;
+    }
+}
+
+// Eight independent accumulators (component x slice parity); fixed pairwise
+// combination order, so the result is deterministic.
+template <int Q, int MODE>
+__device__ __forceinline__ double dist_part_mixed(const double (&x)[Q][4], const float4 (&w)[Q]) {
+    double s[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s[t] = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const float wf[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            double &acc = s[(q & 1) * 4 + c];
+            if (q < PipeSplit<Q>::PQA) {
+                const double wd = (double)wf[c];
+                if (MODE == SOMB_DIST_NAIVE) {
+                    const double a = wd - x[q][c];
+                    acc = __fma_rn(a, a, acc);
+                } else {
+                    acc = __fma_rn(x[q][c], wd, acc);
+                }
+            } else {
+                const double wb = f32_as_f64_scaled(wf[c]);
+                if (MODE == SOMB_DIST_NAIVE) {
+                    const double a = __fma_rn(wb, kF64Scale, -x[q][c]);   // == (double)w - x, one rounding
+                    acc = __fma_rn(a, a, acc);
+                } else {
+                    acc = __fma_rn(x[q][c], wb, acc);                    // (x 2^896)(w 2^-896), exact product
+                }
+            }
+        }
+    }
+    return __dadd_rn(__dadd_rn(__dadd_rn(s[0], s[4]), __dadd_rn(s[1], s[5])),
+                     __dadd_rn(__dadd_rn(s[2], s[6]), __dadd_rn(s[3], s[7])));
+}
 
 template <int Q, int MODE>
 __global__ void __launch_bounds__(32 * RP_WARPS, 3)
@@ -455,8 +522,12 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
 #pragma unroll 1
     for (int64_t wi = (int64_t)blockIdx.x * RP_WARPS + wib; wi < n; wi += (int64_t)gridDim.x * RP_WARPS) {
     const int64_t row = order ? (int64_t)order[wi] : wi;
-    float4 xv[Q];
-    load_row4<Q>(X, row, d4, lane, xv);
+    double xd[Q][4];
+    {
+        float4 xv[Q];
+        load_row4<Q>(X, row, d4, lane, xv);
+        row_operand<Q, MODE>(xv, xd);
+    }
     const int cc = ccount[row];
     const CandLayout L = cand_layout(cc, split, split && ov.ngp ? (int)*ov.ngp : 2);
     int cnt = L.cnt;
@@ -481,14 +552,38 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
     const double xx = x2[row];
     double best = INFINITY;
     int bestj = 0x7fffffff;
-    auto consider = [&](int j, const float4 (&wv)[Q]) {
-        double s = warp_sum(dist_part<Q, MODE>(xv, wv));
-        double v = s;
+    // lane partials of four candidates -> their exact values, folded into
+    // (best, bestj).  A reduce-scatter butterfly: after the xor-16 and xor-8
+    // steps lane L carries candidate ((L >> 4) & 1) * 2 + ((L >> 3) & 1), so
+    // the four sums take 6 fp64 shuffles on one dependency chain instead of
+    // four 5-deep warp_sum chains (the serial shuffle latency was the re-rank's
+    // top stall).  The winner is the lowest (value, index) pair, the same
+    // total order as the one-at-a-time scan.
+    auto consider4 = [&](const double (&p)[4], const int (&jg)[4]) {
+        const bool b4 = lane & 16, b3 = lane & 8;
+        const double a0 = (b4 ? p[2] : p[0]) + __shfl_xor_sync(0xffffffffu, b4 ? p[0] : p[2], 16);
+        const double a1 = (b4 ? p[3] : p[1]) + __shfl_xor_sync(0xffffffffu, b4 ? p[1] : p[3], 16);
+        double c = (b3 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, b3 ? a0 : a1, 8);
+        c += __shfl_xor_sync(0xffffffffu, c, 4);
+        c += __shfl_xor_sync(0xffffffffu, c, 2);
+        c += __shfl_xor_sync(0xffffffffu, c, 1);
+        const int g = (b4 ? 2 : 0) + (b3 ? 1 : 0);
+        const int j = g == 0 ? jg[0] : g == 1 ? jg[1] : g == 2 ? jg[2] : jg[3];
+        const bool ok = (unsigned)j < (unsigned)K;
+        double v = c;
         if (MODE == SOMB_DIST_BLOCKED)   // ((-2 dot) + |x|^2) + |w|^2, clamp (kernels.py:196-202)
-            v = fmax(__dadd_rn(__dadd_rn(__dmul_rn(-2.0, s), xx), w2[(unsigned)j < (unsigned)K ? j : 0]), 0.0);
-        if ((unsigned)j < (unsigned)K && (v < best || (v == best && j < bestj))) {
+            v = fmax(__dadd_rn(__dadd_rn(__dmul_rn(-2.0, c), xx), w2[ok ? j : 0]), 0.0);
+        if (!ok) v = INFINITY;
+        int jj = ok ? j : 0x7fffffff;
+#pragma unroll
+        for (int m = 8; m <= 16; m <<= 1) {
+            const double ov2 = __shfl_xor_sync(0xffffffffu, v, m);
+            const int oj = __shfl_xor_sync(0xffffffffu, jj, m);
+            if (ov2 < v || (ov2 == v && oj < jj)) { v = ov2; jj = oj; }
+        }
+        if (jj != 0x7fffffff && (v < best || (v == best && jj < bestj))) {
             best = v;
-            bestj = j;
+            bestj = jj;
         }
     };
     // one pipelined pass over a candidate list given by get(q), q < m
@@ -499,17 +594,28 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
             cp_async_commit();
         }
 #pragma unroll 1
-        for (int q = 0; q < m; ++q) {
-            const int stg = q % RS;
-            const int j = get(q);
-            const int jn = q + RS < m ? get(q + RS) : -1;
-            cp_async_wait<RS - 1>();
-            float4 wv[Q];
+        for (int q0 = 0; q0 < m; q0 += 4) {
+            double p[4];
+            int jg[4];
 #pragma unroll
-            for (int t = 0; t < Q; ++t) wv[t] = ring[wib][stg][t][lane];
-            if (jn >= 0) issue(jn, stg);
-            cp_async_commit();
-            consider(j, wv);
+            for (int i = 0; i < 4; ++i) {
+                const int q = q0 + i;
+                p[i] = 0.0;
+                jg[i] = -1;
+                if (q < m) {   // warp-uniform
+                    const int stg = q % RS;
+                    jg[i] = get(q);
+                    const int jn = q + RS < m ? get(q + RS) : -1;
+                    cp_async_wait<RS - 1>();
+                    float4 wv[Q];
+#pragma unroll
+                    for (int t = 0; t < Q; ++t) wv[t] = ring[wib][stg][t][lane];
+                    if (jn >= 0) issue(jn, stg);
+                    cp_async_commit();
+                    p[i] = dist_part_mixed<Q, MODE>(xd, wv);
+                }
+            }
+            consider4(p, jg);
         }
         cp_async_wait<0>();
     };
