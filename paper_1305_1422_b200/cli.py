@@ -50,6 +50,8 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--grid", choices=("rectangular", "hexagonal"), default="rectangular")
     p.add_argument("--neighborhood", choices=("gaussian", "bubble"), default="gaussian")
     p.add_argument("--compact-support", action="store_true", help="h = 0 beyond the radius")
+    p.add_argument("--cache", action="store_true",
+                   help="keep a binary copy of the input (INPUT_FILE.sombc) and reuse it while the input is unchanged")
     p.add_argument("input_file", metavar="INPUT_FILE")
     p.add_argument("output_prefix", metavar="OUTPUT_PREFIX")
     return p
@@ -99,7 +101,7 @@ def run(argv) -> int:
     rank, world = _init_distributed()
     from .ingest import read_dataset
     from .train import FileSinks, load_codebook, train
-    data, fmt = read_dataset(ns.input_file)
+    data, fmt = read_dataset(ns.input_file, cache=ns.cache)
     if rank == 0:
         print(f"somb200: read {data.n_vectors} x {data.n_dimensions} {fmt} input from {ns.input_file}"
               + (f" ({world} ranks)" if world > 1 else ""), file=sys.stderr)

@@ -6,6 +6,8 @@ Rows are converted in bulk (one numpy conversion per file, not per row);
 the per-line error checks and messages follow the reference's."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import errors
@@ -171,7 +173,6 @@ def _native_dense(raw: bytes, fmt: str):
     (somb_scan_dense_text / somb_parse_dense_text); None when the input needs
     the reference-exact Python path (errors, unusual tokens, header layout)."""
     import ctypes as C
-    import os
     from . import _lib
     try:
         lib = _lib.load()
@@ -208,10 +209,101 @@ def _native_dense(raw: bytes, fmt: str):
     return DenseDataset(out) if rc == 0 else None
 
 
-def read_dataset(path: str):
+# ------------------------------------------------------------ binary cache
+# INPUT.sombc next to a text input: a 64-byte header (magic, the source's
+# size and mtime_ns, format, kind, n, d, nnz) and the raw arrays (dense f32
+# n x d; CSR int64 offsets, int32 cols, f32 values), read back with one
+# np.fromfile per array.  Stale (source changed) or malformed caches are
+# ignored and rewritten; an unwritable directory just skips the cache.
+_CACHE_MAGIC = b"SOMBC001"
+_FMT_CODES = {"dense": 0, "headered": 1, "sparse": 2}
+
+
+def cache_path(path: str) -> str:
+    return path + ".sombc"
+
+
+def _source_key(path: str):
+    st = os.stat(path)
+    return st.st_size, st.st_mtime_ns
+
+
+def load_cached(path: str):
+    """(dataset, format) from a fresh INPUT.sombc, else None."""
+    cp = cache_path(path)
+    try:
+        size, mtime = _source_key(path)
+        with open(cp, "rb") as fh:
+            head = fh.read(64)
+        if len(head) < 64 or head[:8] != _CACHE_MAGIC:
+            return None
+        src_size, src_mtime, code, kind, n, d, nnz = np.frombuffer(head[8:64], dtype="<i8", count=7)
+        if (int(src_size), int(src_mtime)) != (size, mtime) or n < 0 or d < 0 or nnz < 0:
+            return None
+        fmt = {v: k for k, v in _FMT_CODES.items()}.get(int(code))
+        total = os.path.getsize(cp)
+        if kind == 0:
+            if fmt is None or total != 64 + 4 * n * d:
+                return None
+            vals = np.fromfile(cp, dtype=np.float32, count=int(n * d), offset=64).reshape(int(n), int(d))
+            return DenseDataset(vals), fmt
+        if kind != 1 or fmt is None or total != 64 + 8 * (n + 1) + 8 * nnz:
+            return None
+        offs = np.fromfile(cp, dtype=np.int64, count=int(n + 1), offset=64)
+        cols = np.fromfile(cp, dtype=np.int32, count=int(nnz), offset=64 + 8 * int(n + 1))
+        vals = np.fromfile(cp, dtype=np.float32, count=int(nnz), offset=64 + 8 * int(n + 1) + 4 * int(nnz))
+        return SparseDataset(int(d), offs, cols, vals), fmt
+    except (OSError, ValueError):
+        return None
+
+
+def write_cache(path: str, ds, fmt: str) -> bool:
+    """Write INPUT.sombc atomically (temporary file + rename); False when the
+    directory is not writable."""
+    cp = cache_path(path)
+    tmp = f"{cp}.{os.getpid()}.tmp"
+    try:
+        size, mtime = _source_key(path)
+        sparse = isinstance(ds, SparseDataset)
+        n = ds.n_vectors
+        d = ds.n_dimensions
+        nnz = ds.nnz if sparse else 0
+        head = _CACHE_MAGIC + np.array([size, mtime, _FMT_CODES[fmt], int(sparse), n, d, nnz],
+                                       dtype="<i8").tobytes()
+        with open(tmp, "wb") as fh:
+            fh.write(head)
+            if sparse:
+                fh.write(np.ascontiguousarray(ds.row_offsets, dtype="<i8").tobytes())
+                fh.write(np.ascontiguousarray(ds.col_indices, dtype="<i4").tobytes())
+                fh.write(np.ascontiguousarray(ds.values, dtype="<f4").tobytes())
+            else:
+                np.ascontiguousarray(ds.values, dtype="<f4").tofile(fh)
+        os.replace(tmp, cp)
+        return True
+    except OSError:
+        try:
+            os.unlink(tmp)
+        except OSError:
+            pass
+        return False
+
+
+def read_dataset(path: str, cache: bool = False):
     """(dataset, format) from a file, format auto-detected (fileio.py:305-317).
     Dense bodies go through the native parser; errors and edge cases through
-    the reference-exact Python parsers."""
+    the reference-exact Python parsers.  cache=True reuses / refreshes the
+    binary copy INPUT.sombc (valid while the input's size and mtime match)."""
+    if cache:
+        hit = load_cached(path)
+        if hit is not None:
+            return hit
+    ds, fmt = _read_text(path)
+    if cache:
+        write_cache(path, ds, fmt)
+    return ds, fmt
+
+
+def _read_text(path: str):
     try:
         with open(path, "rb") as fh:
             raw = fh.read()

@@ -101,3 +101,37 @@ def test_native_dense_ingest_matches_python_path(tmp_path):
         b.write_text(bad)
         with pytest.raises(exc):
             ingest.read_dataset(str(b))
+
+
+def test_binary_cache_round_trip_and_staleness(tmp_path, monkeypatch):
+    """read_dataset(cache=True) writes INPUT.sombc, serves the next read from
+    it bit-identically (no text parse), and ignores it once the input changes."""
+    import os
+    rng = np.random.default_rng(3)
+    x = rng.random((257, 9)).astype(np.float32)
+    p = tmp_path / "d.txt"
+    p.write_text("".join(" ".join(repr(float(v)) for v in row) + "\n" for row in x))
+    ds, fmt = ingest.read_dataset(str(p), cache=True)
+    assert os.path.exists(ingest.cache_path(str(p)))
+    calls = []
+    real = ingest._read_text
+    monkeypatch.setattr(ingest, "_read_text", lambda path: calls.append(path) or real(path))
+    ds2, fmt2 = ingest.read_dataset(str(p), cache=True)
+    assert calls == [] and fmt2 == fmt == "dense"
+    np.testing.assert_array_equal(ds2.values, ds.values)
+    s = tmp_path / "s.txt"
+    s.write_text("0:0.5 3:1.25\n\n2:-2 4:3e-3\n")
+    sp, sfmt = ingest.read_dataset(str(s), cache=True)
+    sp2, sfmt2 = ingest.read_dataset(str(s), cache=True)
+    assert sfmt == sfmt2 == "sparse" and len(calls) == 1 and sp2.n_dimensions == sp.n_dimensions
+    for a in ("row_offsets", "col_indices", "values"):
+        np.testing.assert_array_equal(getattr(sp2, a), getattr(sp, a))
+    p.write_text("1 2 3\n4 5 6\n")          # input changed: the cache is stale
+    os.utime(p, ns=(1, 1))
+    ds3, _ = ingest.read_dataset(str(p), cache=True)
+    assert ds3.values.shape == (2, 3) and len(calls) == 2
+    with open(ingest.cache_path(str(p)), "r+b") as fh:   # a damaged cache is ignored
+        fh.write(b"garbage!")
+    ds4, _ = ingest.read_dataset(str(p), cache=True)
+    np.testing.assert_array_equal(ds4.values, ds3.values)
+    assert len(calls) == 3
