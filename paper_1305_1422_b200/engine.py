@@ -59,10 +59,10 @@ def _round_up(v: int, a: int) -> int:
     return (v + a - 1) // a * a
 
 
-_STAGE = {}   # device index -> two cached page-locked staging halves
+_STAGE = {}   # (device index, slot) -> two cached page-locked staging halves
 
 
-def to_host(t: torch.Tensor) -> np.ndarray:
+def to_host(t: torch.Tensor, slot: str = "main") -> np.ndarray:
     """Device -> host copy through two cached page-locked staging buffers: the
     D2H of chunk i+1 overlaps the host copy of chunk i (a pageable copy of the
     160 MB cfg2 codebook runs at ~2 GB/s, and pinning a fresh buffer per call
@@ -74,9 +74,9 @@ def to_host(t: torch.Tensor) -> np.ndarray:
         return out
     chunk = 16 << 20
     dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
-    bufs = _STAGE.get(dev)
-    if bufs is None:
-        bufs = _STAGE[dev] = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    bufs = _STAGE.get((dev, slot))
+    if bufs is None:   # one staging pair per (device, slot): concurrent copies use distinct slots
+        bufs = _STAGE[(dev, slot)] = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
     src = t.view(-1).view(torch.uint8)
     dst = out.reshape(-1).view(np.uint8)
     stream = torch.cuda.current_stream(t.device)
@@ -98,6 +98,7 @@ def to_host(t: torch.Tensor) -> np.ndarray:
 
 
 _POOL = None
+_D2H_POOL = None
 
 
 def _host_copy(dst: int, src: int, nbytes: int, parts: int = 4) -> None:
@@ -287,6 +288,27 @@ class SomEngine:
     def codebook(self) -> np.ndarray:
         return to_host(self.W[: self.K])
 
+    def codebook_async(self):
+        """Future of codebook(): the D2H runs on a side stream (ordered after
+        the work enqueued so far) from a helper thread, so it overlaps what
+        the caller enqueues next -- train() overlaps it with the final BMU
+        pass.  The codebook must not be updated until the future resolves."""
+        global _D2H_POOL
+        if _D2H_POOL is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _D2H_POOL = ThreadPoolExecutor(1)
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.dev)
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(self.dev))
+        W, K, dev, side = self.W, self.K, self.dev, self._side
+
+        def work():
+            with torch.cuda.device(dev), torch.cuda.stream(side):
+                side.wait_event(ready)
+                return to_host(W[:K], slot="side")
+        return _D2H_POOL.submit(work)
+
     # ------------------------------------------------------------- phases
     def prepare(self):
         _lib.call("somb_codebook_prepare_f8" if self.passes == 2 else "somb_codebook_prepare", _ptr(self.W),
@@ -296,6 +318,7 @@ class SomEngine:
 
     # optional per-phase CUDA-event timing (bench.py): name -> [(start, end), ...]
     timing = None
+    _side = None   # side stream of codebook_async (created on first use)
 
     def _mark(self, name, start):
         if self.timing is None:
