@@ -424,3 +424,42 @@ def test_sparse_empty_rows_vs_oracle(screen):
     rel = np.max(np.abs(cb.weights.astype(np.float64) - w) / np.maximum(np.abs(w), 1e-12))
     assert rel <= 1e-4, rel
     assert np.mean(np.any(bmus != bm, axis=1)) <= 1e-2
+
+
+def test_ownership_semantics():
+    """SURVEY 8(b) ownership: inputs are read-only (the given codebook and
+    data are never mutated: test_kernels.py:211-221, test_train.py:130-136),
+    blend returns a new array, init_codebook copies what it is given, and
+    train_wrapper fills the caller's buffers in place
+    (bindings/__init__.py:128-130)."""
+    from paper_1305_1422_b200 import bindings as B
+    rng = np.random.default_rng(5)
+    x = rng.random((300, 7), dtype=np.float32)
+    x0 = x.copy()
+    cfg = S.TrainConfig(n_epochs=2, n_columns=5, n_rows=4)
+    cb = S.init_codebook(cfg, 7)
+    w0 = cb.weights.copy()
+    bmu, qe, acc = S.search_accumulate(S.DenseDataset(x), cb, 2.0, 1e-3, S.MapType.PLANAR,
+                                       S.Kernel.DENSE_BLOCKED)
+    np.testing.assert_array_equal(cb.weights, w0)
+    np.testing.assert_array_equal(x, x0)
+    out = S.blend(cb.weights, acc, 0.5)
+    assert out is not cb.weights and not np.shares_memory(out, cb.weights)
+    np.testing.assert_array_equal(cb.weights, w0)
+    copy = S.init_codebook(cfg, 7, initial_codebook=cb)
+    assert not np.shares_memory(copy.weights, cb.weights)
+    np.testing.assert_array_equal(copy.weights, w0)
+    trained, bm_table, u = S.train(S.DenseDataset(x), cfg, initial_codebook=cb)
+    np.testing.assert_array_equal(cb.weights, w0)
+    np.testing.assert_array_equal(x, x0)
+    # train_wrapper: same training from the seed, outputs written into the caller's arrays
+    ref_cb, ref_bm, ref_u = S.train(S.DenseDataset(x), cfg)
+    flat = x.reshape(-1)
+    cbuf, bbuf, ubuf = np.zeros(20 * 7, np.float32), np.zeros(600, np.int32), np.zeros(20, np.float32)
+    ids = (id(cbuf), id(bbuf), id(ubuf))
+    B.train_wrapper(flat, 2, 5, 4, 7, 300, 0, 0, "linear", 0, 0, "linear", 0, 1, "planar", "", cbuf, bbuf, ubuf)
+    assert ids == (id(cbuf), id(bbuf), id(ubuf))
+    np.testing.assert_array_equal(cbuf, ref_cb.weights.reshape(-1))
+    np.testing.assert_array_equal(bbuf, ref_bm.reshape(-1))
+    np.testing.assert_array_equal(ubuf, ref_u.heights.reshape(-1))
+    np.testing.assert_array_equal(x, x0)
