@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import threading
 from dataclasses import dataclass
 from typing import Optional
 
@@ -59,7 +60,7 @@ def _round_up(v: int, a: int) -> int:
     return (v + a - 1) // a * a
 
 
-_STAGE = {}   # (device index, slot) -> two cached page-locked staging halves
+_STAGE = {}   # (device index, slot, thread) -> two cached page-locked staging halves
 
 
 def to_host(t: torch.Tensor, slot: str = "main") -> np.ndarray:
@@ -74,9 +75,10 @@ def to_host(t: torch.Tensor, slot: str = "main") -> np.ndarray:
         return out
     chunk = 16 << 20
     dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
-    bufs = _STAGE.get((dev, slot))
-    if bufs is None:   # one staging pair per (device, slot): concurrent copies use distinct slots
-        bufs = _STAGE[(dev, slot)] = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    key = (dev, slot, threading.get_ident())
+    bufs = _STAGE.get(key)
+    if bufs is None:   # one staging pair per (device, slot, thread): concurrent copies never share one
+        bufs = _STAGE[key] = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
     src = t.view(-1).view(torch.uint8)
     dst = out.reshape(-1).view(np.uint8)
     stream = torch.cuda.current_stream(t.device)

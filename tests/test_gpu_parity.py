@@ -463,3 +463,34 @@ def test_ownership_semantics():
     np.testing.assert_array_equal(bbuf, ref_bm.reshape(-1))
     np.testing.assert_array_equal(ubuf, ref_u.heights.reshape(-1))
     np.testing.assert_array_equal(x, x0)
+
+
+def test_concurrent_trainings_on_two_streams():
+    """Threading contract: calls are thread-safe per stream --
+    two trainings issued from two host threads, each on its own CUDA stream,
+    give exactly the results of running them one after the other."""
+    import threading
+    rng = np.random.default_rng(9)
+    xs = [rng.random((4000, 24), dtype=np.float32), rng.random((3000, 24), dtype=np.float32)]
+    cfg = S.TrainConfig(n_epochs=3, n_columns=12, n_rows=10)
+    seq = [S.train(S.DenseDataset(x), cfg) for x in xs]
+    out = [None, None]
+    errs = []
+
+    def work(i):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[i] = S.train(S.DenseDataset(xs[i]), cfg)
+                torch.cuda.current_stream().synchronize()
+        except Exception as exc:   # surfaced below
+            errs.append(exc)
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for (cb, bm, u), (cb2, bm2, u2) in zip(seq, out):
+        np.testing.assert_array_equal(cb2.weights, cb.weights)
+        np.testing.assert_array_equal(bm2, bm)
+        np.testing.assert_array_equal(u2.heights, u.heights)
