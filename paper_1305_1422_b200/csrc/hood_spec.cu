@@ -322,6 +322,21 @@ struct MidA {
         return pk ? kr : ki;
     }
 };
+// the same operand materialised once per update as a dense [f][2 nyo][2 ny]
+// array (values bit-identical to MidA), when it fits the workspace budget:
+// the GEMM's A loads become plain loads instead of per-element key math
+struct MidAm {
+    const double *A; int M2, K2;
+    __device__ double operator()(int f, int r, int k) const { return A[((int64_t)f * M2 + r) * K2 + k]; }
+};
+__global__ void spec_mid_mat(MidA a, int F, int M2, int K2, double *__restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)M2 * K2;
+    if (e >= (int64_t)F * per) return;
+    const int f = (int)(e / per), rk = (int)(e % per);
+    out[e] = a(f, rk / K2, rk % K2);
+}
+
 struct MidB {
     SpecGeom g; const double *Sh; int D;
     __device__ double operator()(int f, int k, int d) const {
@@ -407,6 +422,12 @@ static int spec_nkeys(const SpecGeom &g) {
     return g.hex ? 3 * ndy : ndy;
 }
 
+// materialised mid operand (MidAm) for all map rows, if within budget
+static size_t spec_mid_mat_bytes(const SpecGeom &g) {
+    const size_t b = (size_t)g.F * (2 * (size_t)g.ny) * (2 * (size_t)g.ny) * 8;
+    return b <= ((size_t)256 << 20) ? b : 0;
+}
+
 size_t spec_ws_bytes(const somb_map *m, int d) {
     SpecGeom g = spec_geom(m);
     size_t b = 2 * align_up((size_t)g.L * 8, 256);
@@ -414,6 +435,7 @@ size_t spec_ws_bytes(const somb_map *m, int d) {
     b += 2 * align_up((size_t)2 * g.F * g.nx * 8, 256);             // Phi, Psi
     b += align_up((size_t)2 * g.F * g.ny * (d + 1) * 8, 256);      // Shat (+ count channel)
     b += align_up((size_t)2 * g.F * g.ny * (d + 1) * 8, 256);      // Nhat (worst case: all rows)
+    b += align_up(spec_mid_mat_bytes(g), 256);                      // MidAm (0 when over budget)
     return b;
 }
 
@@ -436,6 +458,7 @@ int spec_update(const somb_map *m, const double *htab, const double *S, const do
     double *Sh = (double *)take((size_t)2 * g.F * g.ny * Dp1 * 8);
     const int y0 = j0 / g.nx, y1 = (j1 + g.nx - 1) / g.nx, nyo = y1 - y0;
     double *Nh = (double *)take((size_t)2 * g.F * nyo * Dp1 * 8);
+    double *Am = spec_mid_mat_bytes(g) ? (double *)take(spec_mid_mat_bytes(g)) : nullptr;
     spec_twiddle<<<(g.L + 255) / 256, 256, 0, st>>>(g.L, cs, sn);
     note_launch();
     spec_kernel_table<<<nkeys, 256, (size_t)g.L * 8, st>>>(g, htab, cs, sn, ktab);
@@ -446,8 +469,17 @@ int spec_update(const somb_map *m, const double *htab, const double *S, const do
     note_launch();
     const int nc = den_mode ? Dp1 : d;     // channels carried through the DFTs
     dgemm_launch(g.ny, 2 * g.F, nc, g.nx, FwdA{phi, g.nx}, FwdB{g, S, cnt, d}, FwdEp{g, Sh, Dp1}, st);
-    dgemm_launch(g.F, 2 * nyo, nc, 2 * g.ny, MidA{g, ktT, nkeys, y0, nyo}, MidB{g, Sh, Dp1}, MidEp{g, Nh, nyo, Dp1},
-                 st);
+    if (Am) {
+        const int64_t tot = (int64_t)g.F * (2 * nyo) * (2 * g.ny);
+        spec_mid_mat<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(MidA{g, ktT, nkeys, y0, nyo}, g.F, 2 * nyo,
+                                                                    2 * g.ny, Am);
+        note_launch();
+        dgemm_launch(g.F, 2 * nyo, nc, 2 * g.ny, MidAm{Am, 2 * nyo, 2 * g.ny}, MidB{g, Sh, Dp1},
+                     MidEp{g, Nh, nyo, Dp1}, st);
+    } else {
+        dgemm_launch(g.F, 2 * nyo, nc, 2 * g.ny, MidA{g, ktT, nkeys, y0, nyo}, MidB{g, Sh, Dp1},
+                     MidEp{g, Nh, nyo, Dp1}, st);
+    }
     if (den_mode) {
         spec_den_kernel<<<(nyo * g.nx + 255) / 256, 256, 0, st>>>(g, psi, Nh, nyo, Dp1, y0, j0, j1, tau, den);
         note_launch();
