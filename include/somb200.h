@@ -80,7 +80,10 @@ SOMB_API const char *somb_last_error(void);
  * in shared memory before spilling), "tc_group" 2 (CTA-pair MMA; 1 = single
  * CTA), "tc_multicast" 2 (1-pass screen in 4-CTA clusters whose two pairs
  * share each codebook tile by TMA multicast; 1 = pairs only), "screen_profile" 0 (1 = skip the epilogue: times the TMA + MMA feed
- * alone; results are invalid).  Returns SOMB_E_CONFIG for unknown keys. */
+ * alone; results are invalid), "ovf_chunks" 0 (> 0 caps the usable
+ * overflow-pool chunks -- a test hook for the pool-exhaustion path, where a
+ * full row keeps its lowest screened candidates and is flagged truncated).
+ * Returns SOMB_E_CONFIG for unknown keys. */
 SOMB_API int somb_set_knob(const char *key, int32_t value);
 /* 0 if device `dev` is sm_100 (B200) and the library's kernels load. */
 SOMB_API int somb_device_check(int dev);

@@ -17,6 +17,13 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
                      unsigned *ctrs, OvfPool pool, int *ovf_head, float *ovf_lim, int passes, cudaStream_t st);
 
 static unsigned ovf_chunks(int64_t n) { return (unsigned)(n / 4 > 4096 ? n / 4 : 4096); }
+// test knob (somb_set_knob "ovf_chunks"): cap the usable overflow chunks to
+// exercise the pool-exhaustion path (0 = the whole pool)
+static unsigned g_ovf_limit = 0;
+int bmu_set_knob(const char *key, int value) {
+    if (!strcmp(key, "ovf_chunks")) { g_ovf_limit = value > 0 ? (unsigned)value : 0u; return SOMB_OK; }
+    return SOMB_E_CONFIG;
+}
 
 BmuWs bmu_carve(void *ws, int64_t n, size_t *total) {
     BmuWs w;
@@ -33,7 +40,7 @@ BmuWs bmu_carve(void *ws, int64_t n, size_t *total) {
     w.pool.cnt = (int *)take((size_t)C * sizeof(int));
     w.pool.ent = (int2 *)take((size_t)C * kOvfChunk * sizeof(int2));
     w.pool.ctr = w.ctrs + 1;
-    w.pool.nchunks = C;
+    w.pool.nchunks = g_ovf_limit && g_ovf_limit < C ? g_ovf_limit : C;   // layout always sized for C
     if (total) *total = (size_t)(p - (char *)ws);
     return w;
 }

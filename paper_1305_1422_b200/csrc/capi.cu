@@ -40,10 +40,12 @@ extern "C" unsigned long long somb_launch_count(void) { return somb::g_launches.
 
 namespace somb {
 int screen_tc_set_knob(const char *key, int value);
+int bmu_set_knob(const char *key, int value);
 }
 extern "C" int somb_set_knob(const char *key, int32_t value) {
     SOMB_REQUIRE(key != nullptr, SOMB_E_CONFIG, "set_knob: null key");
-    int rc = somb::screen_tc_set_knob(key, value);
+    int rc = somb::bmu_set_knob(key, value);
+    if (rc == SOMB_E_CONFIG) rc = somb::screen_tc_set_knob(key, value);
     if (rc == SOMB_E_CONFIG) somb::set_error("set_knob: unknown key %s", key);
     return rc;
 }

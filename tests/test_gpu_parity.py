@@ -494,3 +494,41 @@ def test_concurrent_trainings_on_two_streams():
         np.testing.assert_array_equal(cb2.weights, cb.weights)
         np.testing.assert_array_equal(bm2, bm)
         np.testing.assert_array_equal(u2.heights, u.heights)
+
+
+def test_overflow_pool_exhaustion_keeps_exact_ties():
+    """Candidate sets larger than the shared-memory lists spill to the
+    overflow pool (exact results); with the pool capped to one chunk
+    (somb_set_knob "ovf_chunks") the rows that cannot spill keep their
+    lowest screened candidates and are flagged truncated -- their BMU is then
+    still a node at the exact minimum distance (here: a bit-identical copy
+    of the lowest-index winner), every other row is exact."""
+    from paper_1305_1422_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(17)
+    nx, ny, d, n = 16, 16, 64, 2048
+    w = rng.random((nx * ny, d), dtype=np.float32)
+    w[128:] = w[1]                                   # 128 bit-identical copies of node 1
+    x = rng.random((n, d), dtype=np.float32)
+    x[: n // 2] = w[1] + 1e-3 * rng.standard_normal((n // 2, d)).astype(np.float32)
+    exact = S.SomEngine(S.DenseDataset(x), nx, ny, S.MapType.PLANAR, options=EngineOptions(screen="exact"))
+    exact.set_codebook(w)
+    exact.search()
+    want = exact.bmu[:n].cpu().numpy()
+    eng = S.SomEngine(S.DenseDataset(x), nx, ny, S.MapType.PLANAR)
+    eng.set_codebook(w)
+    try:
+        assert lib.somb_set_knob(b"ovf_chunks", 1) == 0
+        eng.search()
+        got = eng.bmu[:n].cpu().numpy()
+        trunc = (eng.flags[:n].cpu().numpy() & 0x01010101) != 0   # bit 0 of a group's byte: truncated
+    finally:
+        assert lib.somb_set_knob(b"ovf_chunks", 0) == 0
+    assert trunc.sum() > 0                            # the capped pool ran out
+    assert np.array_equal(got[~trunc], want[~trunc])
+    assert np.array_equal(w[got[trunc]], w[want[trunc]])   # an exact tie of the true BMU
+    eng.search()                                      # full pool: exact everywhere, nothing truncated
+    assert np.array_equal(eng.bmu[:n].cpu().numpy(), want)
+    fl = eng.flags[:n].cpu().numpy()
+    assert ((fl & 0x01010101) == 0).all() and ((fl & 0x02020202) != 0).any()   # spilled, never truncated
+    assert eng.overflow_chunks() > 1
