@@ -532,3 +532,37 @@ def test_overflow_pool_exhaustion_keeps_exact_ties():
     fl = eng.flags[:n].cpu().numpy()
     assert ((fl & 0x01010101) == 0).all() and ((fl & 0x02020202) != 0).any()   # spilled, never truncated
     assert eng.overflow_chunks() > 1
+
+
+def test_overflow_pool_exhaustion_sparse():
+    """The same contract for the sparse (CSR) screen, which shares the pool."""
+    from paper_1305_1422_b200 import _lib
+    from paper_1305_1422_b200.sparse import SparseEngine
+    lib = _lib.load()
+    rng = np.random.default_rng(19)
+    nx, ny, d, n = 16, 16, 300, 1024
+    w = rng.random((nx * ny, d), dtype=np.float32)
+    w[128:] = w[1]
+    x = rng.random((n, d), dtype=np.float32)
+    x[x < 0.7] = 0.0                                   # ~30% dense rows
+    x[: n // 2] = np.where(x[: n // 2] != 0, w[1], 0.0)
+    data = _csr(x, x != 0)
+    exact = SparseEngine(data, nx, ny, S.MapType.PLANAR, options=EngineOptions(screen="exact"))
+    exact.set_codebook(w)
+    exact.search()
+    want = exact.bmu[:n].cpu().numpy()
+    eng = SparseEngine(data, nx, ny, S.MapType.PLANAR)
+    eng.set_codebook(w)
+    try:
+        assert lib.somb_set_knob(b"ovf_chunks", 1) == 0
+        eng.search()
+        got = eng.bmu[:n].cpu().numpy()
+        trunc = (eng.flags[:n].cpu().numpy() & 0x01010101) != 0
+    finally:
+        assert lib.somb_set_knob(b"ovf_chunks", 0) == 0
+    assert trunc.sum() > 0
+    assert np.array_equal(got[~trunc], want[~trunc])
+    assert np.array_equal(w[got[trunc]], w[want[trunc]])
+    eng.search()
+    assert np.array_equal(eng.bmu[:n].cpu().numpy(), want)
+    assert ((eng.flags[:n].cpu().numpy() & 0x01010101) == 0).all()
