@@ -1,3 +1,5 @@
+"""Candidate counts of the screen with and without the previous-BMU threshold
+seed (engine option seed_prev), on a 20k-row cfg2-shaped run."""
 import os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
