@@ -20,13 +20,19 @@ cfg_name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 n0, d, nx, ny, mt, grid, nbh, compact, desc = bench.CONFIGS[cfg_name]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else n0
 E = int(sys.argv[3]) if len(sys.argv) > 3 else 10
-g = torch.Generator(device="cuda")
-g.manual_seed(1001)
-X = torch.rand((n, d), generator=g, device="cuda")
-data = S.DenseDataset(X)
+sparse = cfg_name == "cfg3"
+if sparse:   # CSR rows of the bench generator; the screened search is the sparse fp16 screen
+    rp, cl, vl = bench.sparse_rows_device(n, d, bench.SPARSE_NNZ, 1001, torch.device("cuda", 0))
+    data = S.SparseDataset(d, rp.cpu().numpy(), cl.cpu().numpy(), vl.cpu().numpy())
+    X = None
+else:
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1001)
+    X = torch.rand((n, d), generator=g, device="cuda")
+    data = S.DenseDataset(X)
 cfg = S.TrainConfig(n_epochs=E, n_columns=nx, n_rows=ny, map_type=S.MapType(mt), grid=S.GridType(grid),
                     neighborhood=S.Neighborhood(nbh), compact_support=compact,
-                    kernel=S.Kernel.DENSE_BLOCKED, seed=1)
+                    kernel=S.Kernel.SPARSE if sparse else S.Kernel.DENSE_BLOCKED, seed=1)
 out = {}
 for screen in ("tensor", "exact"):
     t0 = time.time()
@@ -40,7 +46,7 @@ fb = bt[:, 0].astype(np.int64) * nx + bt[:, 1]
 eb = be[:, 0].astype(np.int64) * nx + be[:, 1]
 bad = np.flatnonzero(fb != eb)
 gap = None
-if len(bad):
+if len(bad) and not sparse:
     W = torch.from_numpy(we).cuda().double()
     xs = X[torch.from_numpy(bad[:20000]).cuda()].double()
     d2 = (xs * xs).sum(1, keepdim=True) + (W * W).sum(1)[None] - 2 * xs @ W.T
