@@ -205,7 +205,7 @@ sp_screen_ls_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ 
                         s_val[w][t] = val[e0 + b0 + t];
                     }
                     __syncwarp();
-#pragma unroll 8
+#pragma unroll 16
                     for (int t = 0; t < m; ++t) {
                         const float v = s_val[w][t];
                         const float4 a = __ldg(reinterpret_cast<const float4 *>(dT + (int64_t)s_col[w][t] * kp + jl));
