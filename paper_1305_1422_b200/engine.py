@@ -46,6 +46,9 @@ class EngineOptions:
     window_kappa2: float = float(os.environ.get("SOMB_WINDOW_KAPPA2", "0.6"))   # 2-pass (fp16 + fp8) window: measured max error ~0.22 units (tools/f8_probe.py)
     conv: str = "auto"                # neighbourhood convolution: "auto", "direct", "spectral"
     rerank_order: bool = True         # re-rank rows in previous-BMU order (L2 locality; same result)
+    shard_update: str = "columns"     # multi-rank update: "columns" (reduce-scatter S by feature columns,
+                                      # each rank updates its columns for all nodes) or "nodes" (all-reduce S,
+                                      # node-slice update, row all-gather)
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -389,16 +392,48 @@ class SomEngine:
                   _ptr(self.S), _ptr(self.cnt), _ptr(self.row_order), _ptr(self.ws), _stream(self.dev))
         self.has_order = True
 
+    def _col_buffers(self):
+        """Staging for the column-sharded exchange (allocated on first use)."""
+        if getattr(self, "_Sr", None) is None:
+            dc, K, P, dev = -(-self.d // self.world), self.K, self.world, self.dev
+            self.dc = dc
+            self._Sst = torch.empty((P, K, dc), dtype=torch.float64, device=dev)
+            self._Sr = torch.empty((K, dc), dtype=torch.float64, device=dev)
+            self._Wst = torch.empty((P, K, dc), dtype=torch.float32, device=dev)
+            self._Wold = torch.zeros((K, dc), dtype=torch.float32, device=dev)
+            self._Wnew = torch.empty((K, dc), dtype=torch.float32, device=dev)
+
     def reduce(self):
         if self.world > 1:
-            from .parallel import allreduce_sum
-            allreduce_sum(self.acc, self.group)
+            from .parallel import allreduce_sum, reduce_scatter_columns
+            if self.opt.shard_update == "columns":
+                # this rank's feature columns of S, summed over ranks; the
+                # counts and qe (the contiguous tail of acc) on every rank
+                self._col_buffers()
+                reduce_scatter_columns(self.S, self.dc, self._Sst, self._Sr, self.group)
+                allreduce_sum(self.acc[self.K * self.d:], self.group)
+            else:
+                allreduce_sum(self.acc, self.group)
 
     def update(self, radius, scale, cutoff, neighborhood=Neighborhood.GAUSSIAN, compact=False,
                num_out=None, den_out=None, all_nodes=False):
         hood = _lib.SombHood(_lib.NBH_BUBBLE if neighborhood is Neighborhood.BUBBLE
                              else _lib.NBH_GAUSSIAN, int(bool(compact)), float(radius), float(cutoff),
                              {"auto": 0, "direct": 1, "spectral": 2}[self.opt.conv], 0)
+        if self.world > 1 and not all_nodes and self.opt.shard_update == "columns":
+            # all nodes, this rank's columns: the update is independent per
+            # feature column, so each column is computed exactly as on one GPU
+            from .parallel import allgather_columns
+            self._col_buffers()
+            a, b = min(self.d, self.rank * self.dc), min(self.d, (self.rank + 1) * self.dc)
+            if b > a:
+                self._Wold[:, : b - a].copy_(self.W[: self.K, a:b])
+            _lib.call("somb_hood_update", _ptr(self._Sr), _ptr(self.cnt), self.dc, C.byref(self.cmap),
+                      C.byref(hood), C.c_double(scale), _ptr(self.dist_tab), _ptr(self._Wold), 0, self.K,
+                      _ptr(self._Wnew), None, None, _ptr(self.ws), _stream(self.dev))
+            allgather_columns(self._Wnew, self._Wst, self.W2[: self.K], self.d, self.group)
+            self.W, self.W2 = self.W2, self.W
+            return
         nb, ne = (0, self.K) if all_nodes else (self.node_begin, self.node_end)
         _lib.call("somb_hood_update", _ptr(self.S), _ptr(self.cnt), self.d, C.byref(self.cmap),
                   C.byref(hood), C.c_double(scale), _ptr(self.dist_tab), _ptr(self.W), nb, ne,

@@ -1,8 +1,11 @@
 """Data-parallel plumbing: the reference's row partition (distributed.py:424-434)
-and per-rank dataset slicing.  The per-epoch exchange (one fp64 all-reduce
-of [S | cnt | qe] + an all-gather of the updated codebook slices) lives in
+and per-rank dataset slicing.  The per-epoch exchange lives in
 engine.SomEngine.reduce / update and replaces the coordinator fold of
-distributed.py:492-514."""
+distributed.py:492-514: a column-block reduce-scatter of the fp64 node sums
+S, an all-reduce of [cnt | qe], every rank's update of its feature columns
+for all nodes, and a column-block all-gather of the new codebook (the
+legacy node-slice scheme -- all-reduce of [S | cnt | qe], node-slice update,
+row all-gather -- stays available as EngineOptions(shard_update="nodes"))."""
 from __future__ import annotations
 
 import numpy as np
@@ -64,3 +67,49 @@ def allgather_rows(buf, rows_per_rank: int, group=None) -> None:
         parts = [torch.empty_like(mine) for _ in range(world)]
         dist.all_gather(parts, mine, group=group)
         buf.copy_(torch.cat(parts, 0))
+
+
+def column_blocks(d: int, p: int) -> list[tuple[int, int]]:
+    """Feature-column ownership: rank r updates columns [r*dc, min(d, (r+1)*dc)), dc = ceil(d/p)."""
+    dc = -(-d // p)
+    return [(min(d, r * dc), min(d, (r + 1) * dc)) for r in range(p)]
+
+
+def reduce_scatter_columns(S, dc: int, staging, out, group=None) -> None:
+    """out [K, dc] <- sum over ranks of this rank's column block of S [K, d]
+    (zero-padded to p*dc columns): S is restaged block-major into `staging`
+    [p, K, dc] so the blocks are contiguous, then reduce-scattered (NCCL; the
+    gloo backend, used by the CPU tests, has no reduce-scatter: all-reduce
+    and take the block)."""
+    import torch.distributed as dist
+    p = staging.shape[0]
+    K, d = S.shape
+    if p * dc > d:
+        staging.zero_()   # padding columns of the last block(s)
+    for r in range(p):
+        a, b = min(d, r * dc), min(d, (r + 1) * dc)
+        if b > a:
+            staging[r, :, : b - a].copy_(S[:, a:b])
+    rank = dist.get_rank(group)
+    if dist.get_backend(group) == "nccl":
+        dist.reduce_scatter_tensor(out, staging, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.all_reduce(staging, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(staging[rank])
+
+
+def allgather_columns(mine, staging, W, d: int, group=None) -> None:
+    """W[:, :d] <- the column blocks [K, dc] of every rank, in rank order."""
+    import torch
+    import torch.distributed as dist
+    p, K, dc = staging.shape
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(staging, mine, group=group)
+    else:
+        parts = [torch.empty_like(mine) for _ in range(p)]
+        dist.all_gather(parts, mine, group=group)
+        staging.copy_(torch.stack(parts, 0))
+    for r in range(p):
+        a, b = min(d, r * dc), min(d, (r + 1) * dc)
+        if b > a:
+            W[:, a:b].copy_(staging[r, :, : b - a])
