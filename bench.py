@@ -410,8 +410,9 @@ def run_ours(args):
                 "config": {"workload": desc, "rows": n, "K": K, "d": d,
                            "schedule": f"{N_EPOCHS}-epoch linear radius {max(min(nx, ny) / 2, 1)}->1, "
                                        f"scale 1->0.01; step s = epoch s mod {N_EPOCHS}",
-                           "parallelism": f"dp{world} (rows sharded, 1 fp64 all-reduce + 1 fp32 "
-                                          f"all-gather per epoch)",
+                           "parallelism": f"dp{world} (rows sharded; per epoch 1 fp64 reduce-scatter of the "
+                                          f"node sums by feature columns, 1 small all-reduce, 1 fp32 all-gather "
+                                          f"of the updated column blocks)",
                            "l2": (f"L2 flushed between timed steps (inputs {in_bytes / 1e6:.0f} MB per GPU, "
                                   f"{L2_FLUSH_BYTES >> 20} MiB buffer written)") if flush else
                                  f"inputs larger than L2 ({in_bytes / 1e9:.2f} GB per GPU)",
