@@ -1,9 +1,10 @@
 """Sharded training through the real CUDA kernels on ONE GPU: two ranks
 (gloo process group, both on cuda:0) run train() on partition(n, 2) slices
-with the per-epoch fp64 all-reduce and codebook all-gather of
-engine.SomEngine, and must reproduce the single-process run (the
+with the per-epoch exchange of engine.SomEngine (column-block
+reduce-scatter of the node sums, [cnt | qe] all-reduce, column all-gather
+of the codebook), and must reproduce the single-process run (the
 reference's distributed equivalence test, test_distributed.py:257-265,
-promises 1e-5; only the fp64 summation order of the all-reduce differs)."""
+promises 1e-5; only the fp64 summation order across ranks differs)."""
 import os
 import socket
 
@@ -22,11 +23,15 @@ def _free_port():
     return port
 
 
-def _cfg(S, kernel):
+def _cfg(S, kernel, big=False):
+    if big:   # >= 2048 nodes: the spectral update; hex toroid, bubble, compact support
+        return S.TrainConfig(n_epochs=4, n_columns=64, n_rows=48, map_type=S.MapType.TOROID, kernel=kernel,
+                             grid=S.GridType.HEXAGONAL, neighborhood=S.Neighborhood.BUBBLE,
+                             compact_support=True)
     return S.TrainConfig(n_epochs=5, n_columns=20, n_rows=16, map_type=S.MapType.TOROID, kernel=kernel)
 
 
-def _worker(rank, world, port, x, sparse, out_dir):
+def _worker(rank, world, port, x, sparse, out_dir, big=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -38,19 +43,19 @@ def _worker(rank, world, port, x, sparse, out_dir):
         else:
             data = S.DenseDataset(x)
             kernel = S.Kernel.DENSE_BLOCKED
-        cb, bmus, u = S.train(data, _cfg(S, kernel), device="cuda:0")
+        cb, bmus, u = S.train(data, _cfg(S, kernel, big), device="cuda:0")
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), w=cb.weights, b=bmus, u=u.heights)
     finally:
         dist.destroy_process_group()
 
 
-def _run(tmp_path, x, sparse):
+def _run(tmp_path, x, sparse, big=False):
     import torch.multiprocessing as mp
     import paper_1305_1422_b200 as S
-    mp.spawn(_worker, args=(2, _free_port(), x, sparse, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), x, sparse, str(tmp_path), big), nprocs=2, join=True)
     data = S.SparseDataset(*x) if sparse else S.DenseDataset(x)
     kernel = S.Kernel.SPARSE if sparse else S.Kernel.DENSE_BLOCKED
-    cb, bmus, u = S.train(data, _cfg(S, kernel), device="cuda:0")
+    cb, bmus, u = S.train(data, _cfg(S, kernel, big), device="cuda:0")
     r0, r1 = np.load(tmp_path / "r0.npz"), np.load(tmp_path / "r1.npz")
     # every rank holds the same replica
     assert np.array_equal(r0["w"], r1["w"]) and np.array_equal(r0["b"], r1["b"])
@@ -67,6 +72,16 @@ def test_sharded_train_dense_two_ranks_one_gpu(tmp_path):
     centers = rng.random((8, 48)).astype(np.float32)
     x = (centers[rng.integers(0, 8, 6000)] + 0.05 * rng.standard_normal((6000, 48))).astype(np.float32)
     _run(tmp_path, x, sparse=False)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+def test_sharded_train_spectral_hex_two_ranks_one_gpu(tmp_path):
+    """3072-node hex toroid (spectral update, bubble, compact support), d = 47:
+    the two column blocks are 24 + 23 columns (one padded)."""
+    rng = np.random.default_rng(6)
+    centers = rng.random((12, 47)).astype(np.float32)
+    x = (centers[rng.integers(0, 12, 8000)] + 0.05 * rng.standard_normal((8000, 47))).astype(np.float32)
+    _run(tmp_path, x, sparse=False, big=True)
 
 
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
