@@ -102,6 +102,37 @@ def to_host(t: torch.Tensor, slot: str = "main") -> np.ndarray:
     return out
 
 
+def to_device(a: np.ndarray, dev) -> torch.Tensor:
+    """Host (pageable numpy) -> device copy through two cached page-locked
+    staging chunks: the threaded host copy of chunk i+1 overlaps the H2D of
+    chunk i, instead of pinning a full-size copy of the array first."""
+    a = np.ascontiguousarray(a)
+    out = torch.empty(a.shape, dtype=torch.from_numpy(np.empty(0, a.dtype)).dtype, device=dev)
+    nbytes = a.nbytes
+    if nbytes < (8 << 20):
+        return out.copy_(torch.from_numpy(a)) if nbytes else out
+    chunk = 32 << 20
+    key = (out.device.index, "up", threading.get_ident())
+    bufs = _STAGE.get(key)
+    if bufs is None:
+        bufs = _STAGE[key] = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    src = a.reshape(-1).view(np.uint8)
+    dst = out.view(-1).view(torch.uint8)
+    stream = torch.cuda.current_stream(out.device)
+    events = [None, None]
+    for i, o in enumerate(range(0, nbytes, chunk)):
+        b = bufs[i % 2]
+        if events[i % 2] is not None:
+            events[i % 2].synchronize()   # the H2D that last read this half is done
+        m = min(chunk, nbytes - o)
+        _host_copy(b.data_ptr(), src.ctypes.data + o, m)
+        dst[o:o + m].copy_(b[:m], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        events[i % 2] = ev
+    return out
+
+
 _POOL = None
 _D2H_POOL = None
 
@@ -241,11 +272,8 @@ class SomEngine:
     def _upload_dense(self, x, dry=False):
         if _is_torch(x):
             xt = x.to(self.dev, dtype=torch.float32, non_blocking=True).contiguous()
-        else:
-            xh = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
-            if not xh.is_pinned():
-                xh = xh.pin_memory()
-            xt = xh.to(self.dev, non_blocking=True)
+        else:   # pageable numpy rows: chunked through cached pinned staging
+            xt = to_device(np.ascontiguousarray(x, dtype=np.float32), self.dev)
         self.X = xt
         self.n, self.d = int(xt.shape[0]), int(xt.shape[1])
         if not dry:

@@ -15,7 +15,7 @@ import torch
 
 from . import _lib, errors
 from .datasets import SparseDataset
-from .engine import SomEngine, _ptr, _round_up, _stream
+from .engine import SomEngine, _ptr, _round_up, _stream, to_device
 
 # rigorous fp32 window for the gather screen: |r~ - r| <= 2 (nnz + 2) 2^-24
 # |x| max|delta| (+ c rounding); the window is twice that bound.
@@ -29,9 +29,9 @@ class SparseEngine(SomEngine):
         if not isinstance(data, SparseDataset):
             raise errors.KernelDataMismatch("SparseEngine needs a SparseDataset")
         dev = self.dev
-        self.rowptr = torch.from_numpy(np.ascontiguousarray(data.row_offsets, np.int64)).to(dev)
-        self.col = torch.from_numpy(np.ascontiguousarray(data.col_indices, np.int32)).to(dev)
-        self.val = torch.from_numpy(np.ascontiguousarray(data.values, np.float32)).to(dev)
+        self.rowptr = to_device(np.ascontiguousarray(data.row_offsets, np.int64), dev)
+        self.col = to_device(np.ascontiguousarray(data.col_indices, np.int32), dev)
+        self.val = to_device(np.ascontiguousarray(data.values, np.float32), dev)
         if self.col.numel() == 0:
             self.col = torch.zeros(1, dtype=torch.int32, device=dev)
             self.val = torch.zeros(1, dtype=torch.float32, device=dev)
