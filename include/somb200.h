@@ -96,12 +96,16 @@ SOMB_API int somb_device_check(int dev);
 SOMB_API size_t somb_data_stats_ws(int32_t d);
 SOMB_API int somb_data_stats(const float *X, int64_t n, int32_t d, float *nu,
                     float *absmax /* [1] max|x - nu| */, void *ws, void *stream);
-/* Xh[i][k] = fp16((x_ik - nu_k) * 2^xexp) (pitch dp, zero pad); Xl (may be
- * NULL) = fp16 residual of that rounding (enables the 3-pass screen);
- * xnorm[i] = |x_i - nu|_2 (f32); x2[i] = |x_i|^2 in fp64 (kernels.py:198). */
+/* Xh[i][k] = fp16((x_ik - nu_k) * 2^xexp) (pitch dp, zero pad), rounded
+ * stochastically (dither hashed from (i, k, value bits)); Xl (may be NULL)
+ * = fp16 residual of a round-to-nearest hi (enables the 3-pass screen);
+ * xnorm[i] = |x_i - nu|_2 (f32); x2[i] = |x_i|^2 in fp64 (kernels.py:198);
+ * xstat[i] (f32 x 4) = {|x'_i|, max_k |x'_ik|, max_k ulp_ik, |ulp_i|_2}, the
+ * row terms of the screening window sigma_i (ulp_ik = the span of the
+ * stochastic rounding of feature k, unscaled). */
 SOMB_API int somb_data_pack(const float *X, int64_t n, int32_t d, const float *nu,
                    int32_t xexp, uint16_t *Xh, uint16_t *Xl, int32_t dp, float *xnorm,
-                   double *x2, void *stream);
+                   double *x2, float *xstat, void *stream);
 
 /* ---- codebook, once per epoch ----------------------------------------
  * mu = mean_j W_j; delta_j = W_j - mu (exact in fp64); Wh = fp16(delta *
@@ -130,7 +134,8 @@ SOMB_API int somb_uniform_f32(uint64_t state_hi, uint64_t state_lo, uint64_t inc
  * max|x - nu|).  The tensor-core screen computes hi.hi (kind::f16) +
  * x_hi8.w_lo8 + x_lo8.w_hi8 (kind::f8f6f4, twice the fp16 rate). */
 SOMB_API int somb_data_pack_f8(const float *X, int64_t n, int32_t d, const float *nu, int32_t xexp,
-                               uint16_t *Xh, uint8_t *X8, int32_t dp, float *xnorm, double *x2, void *stream);
+                               uint16_t *Xh, uint8_t *X8, int32_t dp, float *xnorm, double *x2, float *xstat,
+                               void *stream);
 SOMB_API int somb_codebook_prepare_f8(const float *W, int32_t K, int32_t d, const float *nu, int32_t xexp,
                                       uint16_t *Wh, uint8_t *W8, int32_t dp, int32_t kp, float *c,
                                       double *w2, float *scal, void *ws, void *stream);
@@ -145,7 +150,7 @@ SOMB_API int somb_codebook_prepare_f8(const float *W, int32_t K, int32_t d, cons
  * tcgen05 (sm_100a), 1 = SIMT reference screen (tests), 2 = none (exact
  * scan), 3 = tcgen05 2-pass split (Xl / Wl = the fp8 operands of
  * somb_data_pack_f8 / somb_codebook_prepare_f8). */
-SOMB_API int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xnorm,
+SOMB_API int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xstat,
                    const double *x2, int64_t n, int32_t d, int32_t dp,
                    const uint16_t *Wh, const float *W, const float *c,
                    const double *w2, int32_t K, int32_t kp, const float *scal,
@@ -159,14 +164,20 @@ SOMB_API size_t somb_bmu_ws(int64_t n);
 /* prev_bmu (may be NULL): each row's BMU from the previous search; seeds the
  * screening threshold (does not change the result, only the work). */
 /* Xl / Wl (both non-NULL): 3-pass split screen hi.hi + hi.lo + lo.hi. */
-SOMB_API int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm, int64_t n,
+SOMB_API int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const float *xstat, int64_t n,
                              int32_t dp, const uint16_t *Wh, const uint16_t *Wl, const float *c,
                              int32_t K, int32_t kp, const float *scal,
                              float window_coef, const int32_t *prev_bmu,
                              int32_t screen_impl, int32_t *flags, void *ws,
                              void *stream);
+/* Rows of the last somb_bmu_screen / somb_bmu_sparse whose candidate set
+ * was truncated (overflow pool exhausted) and therefore re-ranked by an
+ * exact scan of every node instead (the result stays the reference's
+ * argmin).  Reads a device counter in ws: synchronises `stream`; -1 on a
+ * CUDA error. */
+SOMB_API int64_t somb_bmu_repaired_rows(const void *ws, int64_t n, void *stream);
 /* Calibration: tcgen05 screened values of rows [0, min(n,128)) x kp nodes. */
-SOMB_API int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm,
+SOMB_API int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, const float *xstat,
                                     int64_t n, int32_t dp, const uint16_t *Wh, const uint16_t *Wl,
                                     const float *c, int32_t kp, const float *scal,
                                     float window_coef, int32_t passes, float *dump, void *ws,
@@ -184,7 +195,7 @@ SOMB_API int somb_bmu_rerank(const float *X, const double *x2, int64_t n,
 /* The whole BMU search in one call: somb_bmu_screen (seeded from
  * prev_bmu, may be NULL) + somb_bmu_rerank (visiting rows in row_order,
  * may be NULL).  ws >= somb_bmu_ws(n). */
-SOMB_API int somb_bmu_search(const uint16_t *Xh, const uint16_t *Xl, const float *X, const float *xnorm,
+SOMB_API int somb_bmu_search(const uint16_t *Xh, const uint16_t *Xl, const float *X, const float *xstat,
                              const double *x2, int64_t n, int32_t d, int32_t dp, const uint16_t *Wh,
                              const uint16_t *Wl, const float *W, const float *c, const double *w2,
                              int32_t K, int32_t kp, const float *scal, float window_coef,

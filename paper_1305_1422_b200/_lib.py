@@ -47,7 +47,7 @@ SIGNATURES = {
     "somb_device_check": (C.c_int, [C.c_int]),
     "somb_data_stats_ws": (SZ, [I32]),
     "somb_data_stats": (C.c_int, [P, I64, I32, P, P, P, P]),
-    "somb_data_pack": (C.c_int, [P, I64, I32, P, I32, P, P, I32, P, P, P]),
+    "somb_data_pack": (C.c_int, [P, I64, I32, P, I32, P, P, I32, P, P, P, P]),
     "somb_codebook_ws": (SZ, [I32, I32]),
     "somb_codebook_prepare": (C.c_int, [P, I32, I32, P, I32, P, P, I32, I32, P, P, P, P, P]),
     "somb_bmu_ws": (SZ, [I64]),
@@ -55,12 +55,13 @@ SIGNATURES = {
                                  I32, I32, P, P, P, P, P]),
     "somb_bmu_screen": (C.c_int, [P, P, P, I64, I32, P, P, P, I32, I32, P, F32, P, I32, P, P, P]),
     "somb_debug_screen_dump": (C.c_int, [P, P, P, I64, I32, P, P, P, I32, P, F32, I32, P, P, P]),
-    "somb_data_pack_f8": (C.c_int, [P, I64, I32, P, I32, P, P, I32, P, P, P]),
+    "somb_data_pack_f8": (C.c_int, [P, I64, I32, P, I32, P, P, I32, P, P, P, P]),
     "somb_codebook_prepare_f8": (C.c_int, [P, I32, I32, P, I32, P, P, I32, I32, P, P, P, P, P]),
     "somb_bmu_rerank": (C.c_int, [P, P, I64, I32, P, P, I32, I32, I32, P, P, P, P, P, P]),
     "somb_bmu_search": (C.c_int, [P, P, P, P, P, I64, I32, I32, P, P, P, P, P, I32, I32, P, F32, P, P, I32,
                                   I32, P, P, P, P, P]),
     "somb_qe_sum": (C.c_int, [P, I64, P, P, P]),
+    "somb_bmu_repaired_rows": (I64, [P, I64, P]),
     "somb_launch_count": (C.c_ulonglong, []),
     "somb_format_f32_rows": (I64, [P, I64, I64, P, I64, I32]),
     "somb_format_bmus": (I64, [P, I64, P, I64, I32]),

@@ -24,7 +24,7 @@ class _Parser(argparse.ArgumentParser):
 
 
 def build_parser() -> argparse.ArgumentParser:
-    p = _Parser(prog="somb200", description="B200 batch self-organizing map trainer")
+    p = _Parser(prog="somb200", description="B200 batch self-organizing map trainer", allow_abbrev=False)
     p.add_argument("-c", "--initial-codebook", metavar="FILE", default=None,
                    help="initial codebook file (default: seeded random init)")
     p.add_argument("-e", "--epochs", type=int, default=10, metavar="N", help="training epochs (default 10)")

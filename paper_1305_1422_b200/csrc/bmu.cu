@@ -12,11 +12,15 @@
 namespace somb {
 
 int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh,
-                     const __half *Wl, int kp, const float *c, const float *xnorm, const float *scal,
+                     const __half *Wl, int kp, const float *c, const float *xstat, const float *scal,
                      float wcoef, const float *thr0, int *cand, int *ccount, int *flags, float *dump,
                      unsigned *ctrs, OvfPool pool, int *ovf_head, float *ovf_lim, int passes, cudaStream_t st);
 
-static unsigned ovf_chunks(int64_t n) { return (unsigned)(n / 4 > 4096 ? n / 4 : 4096); }
+// overflow pool: 4 chunks (128 spilled candidates) per row on average on top
+// of the 64 shared-memory slots -- near-constant or clustered data keeps
+// 100-200 nodes per row inside the window (profiles/r2_window_calib_*.json);
+// rows beyond the pool are truncated and repaired by an exact scan
+static unsigned ovf_chunks(int64_t n) { return (unsigned)(4 * n > 4096 ? 4 * n : 4096); }
 // test knob (somb_set_knob "ovf_chunks"): cap the usable overflow chunks to
 // exercise the pool-exhaustion path (0 = the whole pool)
 static unsigned g_ovf_limit = 0;
@@ -33,7 +37,7 @@ BmuWs bmu_carve(void *ws, int64_t n, size_t *total) {
     w.cand = (int *)take((size_t)n * SOMB_CAND_CAP * sizeof(int));
     w.ccount = (int *)take((size_t)n * sizeof(int));
     w.thr0 = (float *)take((size_t)n * sizeof(float));
-    w.ctrs = (unsigned *)take(4 * sizeof(unsigned));
+    w.ctrs = (unsigned *)take(8 * sizeof(unsigned));
     w.ovf_head = (int *)take((size_t)4 * n * sizeof(int));
     w.ovf_lim = (float *)take((size_t)4 * n * sizeof(float));
     w.pool.next = (int *)take((size_t)C * sizeof(int));
@@ -43,6 +47,32 @@ BmuWs bmu_carve(void *ws, int64_t n, size_t *total) {
     w.pool.nchunks = g_ovf_limit && g_ovf_limit < C ? g_ovf_limit : C;   // layout always sized for C
     if (total) *total = (size_t)(p - (char *)ws);
     return w;
+}
+
+// Exact repair of truncated rows: a row whose candidate set was cut (the
+// overflow pool ran out, cand.cuh) may have lost its true BMU, so its list
+// is emptied and the re-rank scans every node for it in fp64 -- the result
+// is the reference's argmin (kernels.py:195-205, first-minimum ties 27-28)
+// for every row, truncated or not.  flags: bit 0 of any byte = truncated
+// (one byte per column group of the tcgen05 screen, one word otherwise);
+// ctr counts the repaired rows (ws counter 4, somb_bmu_repaired_rows).
+__global__ void repair_truncated_kernel(const int *__restrict__ flags, int *__restrict__ ccount, int64_t n,
+                                        unsigned *__restrict__ ctr) {
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n) return;
+    if (flags[row] & 0x01010101) {
+        ccount[row] = 0;
+        atomicAdd(ctr, 1u);
+    }
+}
+
+int launch_repair_truncated(const int *flags, int *ccount, int64_t n, unsigned *ctrs, cudaStream_t st) {
+    cudaMemsetAsync(ctrs + 4, 0, sizeof(unsigned), st);
+    if (n == 0) return SOMB_OK;
+    repair_truncated_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flags, ccount, n, ctrs + 4);
+    note_launch();
+    SOMB_LAUNCH_CHECK("repair_truncated");
+    return SOMB_OK;
 }
 
 // Spilled candidates of one row (tcgen05 screen overflow lists), read by the re-rank.
@@ -104,7 +134,7 @@ __device__ __forceinline__ double e4m3_to_double(uint8_t b) {
 // hi.hi + cross products, slack 1.5 windows as for the 3-pass screen.
 __global__ void screen_seed_kernel(const __half *__restrict__ Xh, const __half *__restrict__ Xl, int64_t n, int dp,
                                    const __half *__restrict__ Wh, const __half *__restrict__ Wl, int K,
-                                   const float *__restrict__ c, const float *__restrict__ xnorm,
+                                   const float *__restrict__ c, const float *__restrict__ xstat,
                                    const float *__restrict__ scal, float wcoef, const int *__restrict__ prev,
                                    float *__restrict__ thr0, int f8) {
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -115,7 +145,7 @@ __global__ void screen_seed_kernel(const __half *__restrict__ Xh, const __half *
     if (j >= 0 && j < K) {
         const __half2 *x = reinterpret_cast<const __half2 *>(Xh + row * (int64_t)dp);
         const __half2 *w = reinterpret_cast<const __half2 *>(Wh + (int64_t)j * dp);
-        float win = wcoef * xnorm[row] * scal[1];
+        float win = wcoef * screen_sigma(reinterpret_cast<const float4 *>(xstat)[row], scal);
         float r;
         if (f8) {
             const uint8_t *x8 = reinterpret_cast<const uint8_t *>(Xl) + row * (int64_t)(2 * dp);
@@ -169,7 +199,7 @@ constexpr int kSimtCap = 32;   // candidates per row of the reference screen (<=
 
 __global__ void __launch_bounds__(kSimtRows)
 screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __half *__restrict__ Wh,
-                   int kp, const float *__restrict__ c, const float *__restrict__ xnorm,
+                   int kp, const float *__restrict__ c, const float *__restrict__ xstat,
                    const float *__restrict__ scal, float wcoef, const float *__restrict__ thr0,
                    int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags) {
     __shared__ float wt[kSimtCols][kSimtK + 1];
@@ -179,9 +209,8 @@ screen_simt_kernel(const __half *__restrict__ Xh, int64_t n, int dp, const __hal
     const int64_t row = (int64_t)blockIdx.x * kSimtRows + t;
     const bool live = row < n;
     const float m = scal[0];
-    const float nmax = scal[1];
     CandRow<kSimtCap> st;
-    cand_init(st, live ? wcoef * xnorm[row] * nmax : 0.0f);
+    cand_init(st, live ? wcoef * screen_sigma(reinterpret_cast<const float4 *>(xstat)[row], scal) : 0.0f);
     if (live && thr0) st.thr = thr0[row];
     const CandBuf cb{smem_addr(bv + t), smem_addr(bi + t), 4u * kSimtRows};
     const __half *xr = Xh + (live ? row : 0) * (int64_t)dp;
@@ -727,7 +756,7 @@ extern "C" size_t somb_bmu_ws(int64_t n) {
     return total + 256;
 }
 
-extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm, int64_t n, int32_t dp,
+extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const float *xstat, int64_t n, int32_t dp,
                                const uint16_t *Wh, const uint16_t *Wl, const float *c, int32_t K, int32_t kp,
                                const float *scal, float window_coef, const int32_t *prev_bmu,
                                int32_t screen_impl, int32_t *flags, void *ws, void *stream) {
@@ -744,21 +773,24 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
         const bool split = Xl != nullptr && Wl != nullptr && (screen_impl == 0 || screen_impl == 3);
         screen_seed_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(
             (const __half *)Xh, split ? (const __half *)Xl : nullptr, n, dp, (const __half *)Wh,
-            split ? (const __half *)Wl : nullptr, K, c, xnorm, scal, window_coef, prev_bmu, thr0,
+            split ? (const __half *)Wl : nullptr, K, c, xstat, scal, window_coef, prev_bmu, thr0,
             screen_impl == 3);
         note_launch();
     }
-    if (screen_impl == 0 || screen_impl == 3)
-        return launch_screen_tc((const __half *)Xh, (const __half *)Xl, n, dp, (const __half *)Wh,
-                                (const __half *)Wl, kp, c, xnorm, scal, window_coef, thr0, cand, ccount, flags,
-                                nullptr, w.ctrs, w.pool, w.ovf_head, w.ovf_lim,
-                                screen_impl == 3 ? 2 : (Xl && Wl ? 3 : 1), st);
-    unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
-    screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh, kp, c,
-                                                      xnorm, scal, window_coef, thr0, cand, ccount, flags);
-    note_launch();
-    SOMB_LAUNCH_CHECK("screen_simt");
-    return SOMB_OK;
+    if (screen_impl == 0 || screen_impl == 3) {
+        int rc = launch_screen_tc((const __half *)Xh, (const __half *)Xl, n, dp, (const __half *)Wh,
+                                  (const __half *)Wl, kp, c, xstat, scal, window_coef, thr0, cand, ccount, flags,
+                                  nullptr, w.ctrs, w.pool, w.ovf_head, w.ovf_lim,
+                                  screen_impl == 3 ? 2 : (Xl && Wl ? 3 : 1), st);
+        if (rc) return rc;
+    } else {
+        unsigned blocks = (unsigned)((n + kSimtRows - 1) / kSimtRows);
+        screen_simt_kernel<<<blocks, kSimtRows, 0, st>>>((const __half *)Xh, n, dp, (const __half *)Wh, kp, c,
+                                                          xstat, scal, window_coef, thr0, cand, ccount, flags);
+        note_launch();
+        SOMB_LAUNCH_CHECK("screen_simt");
+    }
+    return launch_repair_truncated(flags, ccount, n, w.ctrs, st);
 }
 
 static int g_rerank_pipe = -1;   // SOMB_RERANK_PIPE=0 selects the unpipelined kernel (A/B testing)
@@ -811,7 +843,7 @@ extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int3
     return SOMB_OK;
 }
 
-extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xnorm, const double *x2,
+extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *xstat, const double *x2,
                               int64_t n, int32_t d, int32_t dp, const uint16_t *Wh, const float *W,
                               const float *c, const double *w2, int32_t K, int32_t kp,
                               const float *scal, float window_coef, int32_t dist_mode,
@@ -819,10 +851,22 @@ extern "C" int somb_bmu_dense(const uint16_t *Xh, const float *X, const float *x
                               void *ws, void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && kp >= K, SOMB_E_INPUT,
                  "bmu_dense: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
-    int rc = somb_bmu_screen(Xh, nullptr, xnorm, n, dp, Wh, nullptr, c, K, kp, scal, window_coef, nullptr,
+    int rc = somb_bmu_screen(Xh, nullptr, xstat, n, dp, Wh, nullptr, c, K, kp, scal, window_coef, nullptr,
                              screen_impl, flags, ws, stream);
     if (rc) return rc;
     return somb_bmu_rerank(X, x2, n, d, W, w2, K, dist_mode, screen_impl, nullptr, bmu, d2min, flags, ws, stream);
+}
+
+extern "C" int64_t somb_bmu_repaired_rows(const void *ws, int64_t n, void *stream) {
+    // rows of the last screen whose truncated candidate set was replaced by
+    // an exact full scan (host read: synchronises the stream)
+    BmuWs w = bmu_carve(const_cast<void *>(ws), n);
+    unsigned v = 0;
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemcpyAsync(&v, w.ctrs + 4, sizeof(unsigned), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return -1;
+    return (int64_t)v;
 }
 
 extern "C" int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws, void *stream) {
@@ -844,7 +888,7 @@ extern "C" int somb_qe_sum(const double *d2min, int64_t n, double *out, void *ws
 // Debug/calibration: screened values r_j of rows [0, min(n, 128)) for all kp
 // nodes from the tcgen05 kernel (dump [128][kp] f32); candidates are
 // computed as usual.  Used to measure the real screen error.
-extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, const float *xnorm, int64_t n,
+extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, const float *xstat, int64_t n,
                                       int32_t dp, const uint16_t *Wh, const uint16_t *Wl, const float *c, int32_t kp,
                                       const float *scal, float window_coef, int32_t passes, float *dump, void *ws,
                                       void *stream) {
@@ -852,13 +896,13 @@ extern "C" int somb_debug_screen_dump(const uint16_t *Xh, const uint16_t *Xl, co
     BmuWs w = bmu_carve(ws, n);
     int *flags = (int *)w.thr0;
     return launch_screen_tc((const __half *)Xh, (const __half *)Xl, m, dp, (const __half *)Wh, (const __half *)Wl, kp,
-                            c, xnorm, scal, window_coef, nullptr, w.cand, w.ccount, flags, dump, w.ctrs, w.pool,
+                            c, xstat, scal, window_coef, nullptr, w.cand, w.ccount, flags, dump, w.ctrs, w.pool,
                             w.ovf_head, w.ovf_lim, passes, as_stream(stream));
 }
 
 
 // Full BMU search in one call: previous-BMU seed + screen + exact re-rank.
-extern "C" int somb_bmu_search(const uint16_t *Xh, const uint16_t *Xl, const float *X, const float *xnorm,
+extern "C" int somb_bmu_search(const uint16_t *Xh, const uint16_t *Xl, const float *X, const float *xstat,
                                const double *x2, int64_t n, int32_t d, int32_t dp, const uint16_t *Wh,
                                const uint16_t *Wl, const float *W, const float *c, const double *w2, int32_t K,
                                int32_t kp, const float *scal, float window_coef, const int32_t *prev_bmu,
@@ -866,7 +910,7 @@ extern "C" int somb_bmu_search(const uint16_t *Xh, const uint16_t *Xl, const flo
                                double *d2min, int32_t *flags, void *ws, void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0 && dp >= d && dp % 8 == 0 && kp >= K && kp % 256 == 0, SOMB_E_INPUT,
                  "bmu_search: bad shape K=%d d=%d dp=%d kp=%d", K, d, dp, kp);
-    int rc = somb_bmu_screen(Xh, Xl, xnorm, n, dp, Wh, Wl, c, K, kp, scal, window_coef, prev_bmu, screen_impl, flags,
+    int rc = somb_bmu_screen(Xh, Xl, xstat, n, dp, Wh, Wl, c, K, kp, scal, window_coef, prev_bmu, screen_impl, flags,
                              ws, stream);
     if (rc) return rc;
     return somb_bmu_rerank(X, x2, n, d, W, w2, K, dist_mode, screen_impl, row_order, bmu, d2min, flags, ws, stream);

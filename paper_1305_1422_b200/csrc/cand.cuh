@@ -74,7 +74,7 @@ struct OvfPool {
 
 // BMU workspace (bmu.cu): cand [n][CAP] int | ccount [n] int | thr0 [n]
 // float | counters | overflow: head [2n] int, lim [2n] float, next [C],
-// cnt [C], entries [C][32] int2 with C = max(4096, n / 4) chunks.
+// cnt [C], entries [C][32] int2 with C = max(4096, 4 n) chunks.
 struct BmuWs {
     int *cand, *ccount;
     float *thr0;
@@ -96,6 +96,27 @@ __device__ __forceinline__ int cb_ldi(const CandBufG &b, int e) { return b.i[e];
 __device__ __forceinline__ void cb_st(const CandBufG &b, int e, float v, int j) {
     b.v[e] = v;
     b.i[e] = j;
+}
+
+// Per-row scale sigma_i of the dense screen's error.  The
+// fp16 operands are rounded stochastically (prep.cu), so the error of
+// x~_i . delta~_j is a sum over features of independent mean-zero terms,
+// sum_k e_ik delta_jk + x'_ik f_jk (+ e f), with |e_ik| < ulp_ik and
+// |f_jk| < ulp(delta_jk).  Its Hoeffding scale
+// sqrt(sum_k ulp_ik^2 delta_jk^2 + x'_ik^2 ulp(delta_jk)^2) is bounded per
+// row, for every node j, by two Hoelder forms per term:
+//   x side: min(max_k ulp_ik * max_j|delta_j|, |ulp_i|_2 * max_jk|delta_jk|)
+//   delta side: min(max_k|x'_ik| * max_j|ulp(delta_j)|_2, |x'_i| * max ulp(delta))
+// plus a 2^-20 slack for the fp32 rounding of c_j and of r~ (|r| <= |c| +
+// 2 |x'| |delta|).  xs = xstat[row] = {|x'|, max|x'_k|, max ulp_k, |ulp|_2}
+// (somb_data_pack); scal[1] = max_j|delta_j|, scal[3] = max_jk|delta_jk|,
+// scal[4] = max|c_j|, scal[5] = max_j|ulp(delta_j)|_2, scal[6] = max ulp
+// (somb_codebook_prepare).  The screening window of a row is
+// window_coef * sigma_i (1-pass: 5, 2-pass fp8 cross terms: 0.5; engine.py).
+__device__ __forceinline__ float screen_sigma(float4 xs, const float *__restrict__ scal) {
+    const float sx = fminf(xs.z * scal[1], xs.w * scal[3]);
+    const float sd = fminf(xs.y * scal[5], xs.x * scal[6]);
+    return sqrtf(sx * sx + sd * sd) + ldexpf(scal[4] + 2.0f * xs.x * scal[1], -20);
 }
 
 template <int CAP>

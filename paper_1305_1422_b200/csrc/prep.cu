@@ -9,10 +9,60 @@
 // relative to the gaps between nodes after the codebook collapses
 // (SURVEY.md 7.3-1).
 #include <cuda_fp8.h>
+#include <float.h>
 
 #include "common.cuh"
 
 namespace somb {
+
+
+// ----------------------------------------------------- stochastic rounding
+// The screen's fp16 operands are rounded STOCHASTICALLY:
+// v goes to the fp16 neighbour above |v| with probability (|v| - lo) / ulp,
+// using 32 dither bits from a counter-based hash of (row or node, feature,
+// value bits).  The rounding errors are then independent and mean-zero
+// whatever the data's structure (constant rows, duplicated columns, integer
+// values), so the screen error is a sum of independent terms whose scale
+// the per-row window sigma (screen_sigma, cand.cuh) bounds from the rows'
+// ulp profile.  Round-to-nearest made them coherent on such data (a
+// near-constant row rounds every feature the same way), which broke a
+// window calibrated on uniform data (Weak 1).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+__device__ __forceinline__ uint32_t dither32(uint64_t domain, uint64_t a, uint32_t b, uint32_t vbits) {
+    uint64_t z = mix64(domain ^ (a * 0x9E3779B97F4A7C15ull));
+    z = mix64(z ^ (((uint64_t)b << 32) | vbits));
+    return (uint32_t)(z >> 32);
+}
+constexpr uint64_t kDitherX = 0x5EEDDA7A00000001ull;   // data rows
+constexpr uint64_t kDitherW = 0x5EEDC0DE00000002ull;   // codebook nodes
+
+// fp16 spacing at |v| (normal range; subnormal spacing 2^-24) and whether v
+// sits exactly on the grid (then it rounds without error)
+__device__ __forceinline__ double f16_spacing(double a) {
+    int e = ilogb(a);
+    return ldexp(1.0, (e < -14 ? -14 : e) - 10);
+}
+
+// Stochastic rounding of v (|v| < 65504) to fp16; *err_span = the spacing
+// of the two candidates (the width of the error's range), 0 if v is exact.
+__device__ __forceinline__ __half sr_half(double v, uint32_t u, double *err_span) {
+    const double a = fabs(v);
+    if (a == 0.0) { *err_span = 0.0; return __double2half(0.0); }
+    const double sp = f16_spacing(a);
+    const double q = a / sp;                 // exact: power-of-two scaling
+    const double fl = floor(q);
+    const double fr = q - fl;                // exact
+    *err_span = fr > 0.0 ? sp : 0.0;
+    const double m = fl + (ldexp((double)u, -32) < fr ? 1.0 : 0.0);
+    return __double2half(copysign(m * sp, v));   // exactly representable
+}
 
 // ---------------------------------------------------------------- data stats
 // Stage 1: per (row-chunk, column) fp64 partial sum plus column min/max.
@@ -58,13 +108,18 @@ __global__ void data_stats_final(const double *__restrict__ psum, const float *_
     atomic_max_nonneg(absmax, a);
 }
 
-// Xh = fp16((x - nu) * 2^xexp), xnorm = |x - nu|, x2 = |x|^2 (fp64).
-// Optional Xl = fp16 residual (v * 2^xexp - Xh): with it the screen runs the
-// 3-pass split product hi.hi + hi.lo + lo.hi (~22-bit operands).
+// Xh = fp16((x - nu) * 2^xexp) (stochastic rounding), xnorm = |x - nu|,
+// x2 = |x|^2 (fp64), xstat = {|x'|, max_k |x'_k|, max_k ulp_k, |ulp|_2}
+// with ulp_k the error span of feature k (unscaled units): the row inputs of
+// the window sigma.  With Xl (3-pass screen): round-to-nearest hi and the
+// fp16 residual Xl (~22-bit operands, hi.hi + hi.lo + lo.hi); its window is
+// the accumulation-bound unit 2^-11 |x'| max|delta| / sqrt(d), which xstat
+// encodes as {|x'|, 0, |x'| 2^-11 / sqrt(d), FLT_MAX} (screen_sigma).
 __global__ void data_pack_kernel(const float *__restrict__ X, int64_t n, int d,
                                  const float *__restrict__ nu, int xexp,
                                  __half *__restrict__ Xh, __half *__restrict__ Xl, int dp,
-                                 float *__restrict__ xnorm, double *__restrict__ x2) {
+                                 float *__restrict__ xnorm, double *__restrict__ x2,
+                                 float4 *__restrict__ xstat) {
     int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     int lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -72,16 +127,27 @@ __global__ void data_pack_kernel(const float *__restrict__ X, int64_t n, int d,
     __half *o = Xh + row * dp;
     __half *ol = Xl ? Xl + row * dp : nullptr;
     double sc = ldexp(1.0, xexp);
-    double nrm = 0.0, sq = 0.0;
+    double nrm = 0.0, sq = 0.0, u2 = 0.0;
+    float xinf = 0.0f, uinf = 0.0f;
     for (int k = lane; k < dp; k += 32) {
         if (k < d) {
-            double xv = (double)x[k];
+            const float xf = x[k];
+            double xv = (double)xf;
             double v = xv - (double)nu[k];
             nrm += v * v;
             sq += xv * xv;
-            __half h = __double2half(v * sc);
-            o[k] = h;
-            if (ol) ol[k] = __double2half(v * sc - (double)__half2float(h));
+            xinf = fmaxf(xinf, (float)fabs(v));
+            if (ol) {
+                __half h = __double2half(v * sc);
+                o[k] = h;
+                ol[k] = __double2half(v * sc - (double)__half2float(h));
+            } else {
+                double span;
+                o[k] = sr_half(v * sc, dither32(kDitherX, (uint64_t)row, (uint32_t)k, __float_as_uint(xf)), &span);
+                span = ldexp(span, -xexp);
+                u2 += span * span;
+                uinf = fmaxf(uinf, (float)span);
+            }
         } else {
             o[k] = __double2half(0.0);
             if (ol) ol[k] = __double2half(0.0);
@@ -89,9 +155,16 @@ __global__ void data_pack_kernel(const float *__restrict__ X, int64_t n, int d,
     }
     nrm = warp_sum(nrm);
     sq = warp_sum(sq);
+    u2 = warp_sum(u2);
+    xinf = warp_max(xinf);
+    uinf = warp_max(uinf);
     if (lane == 0) {
-        xnorm[row] = (float)sqrt(nrm);
+        const float xn = (float)sqrt(nrm);
+        xnorm[row] = xn;
         x2[row] = sq;
+        if (xstat)
+            xstat[row] = ol ? make_float4(xn, 0.0f, xn * (float)ldexp(rsqrt((double)d), -11), FLT_MAX)
+                            : make_float4(xn, xinf, uinf, (float)sqrt(u2));
     }
 }
 
@@ -105,7 +178,7 @@ __device__ __forceinline__ uint8_t to_e4m3(double v) {
 
 __global__ void data_pack_f8_kernel(const float *__restrict__ X, int64_t n, int d, const float *__restrict__ nu,
                                     int xexp, __half *__restrict__ Xh, uint8_t *__restrict__ X8, int dp,
-                                    float *__restrict__ xnorm, double *__restrict__ x2) {
+                                    float *__restrict__ xnorm, double *__restrict__ x2, float4 *__restrict__ xstat) {
     int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     int lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -113,16 +186,24 @@ __global__ void data_pack_f8_kernel(const float *__restrict__ X, int64_t n, int 
     __half *o = Xh + row * dp;
     uint8_t *o8 = X8 + row * (int64_t)(2 * dp);
     const double sc = ldexp(1.0, xexp);
-    double nrm = 0.0, sq = 0.0;
+    double nrm = 0.0, sq = 0.0, u2 = 0.0;
+    float xinf = 0.0f, uinf = 0.0f;
     for (int k = lane; k < dp; k += 32) {
         double v = 0.0;
+        __half h = __double2half(0.0);
         if (k < d) {
-            double xv = (double)x[k];
+            const float xf = x[k];
+            double xv = (double)xf;
             v = xv - (double)nu[k];
             nrm += v * v;
             sq += xv * xv;
+            xinf = fmaxf(xinf, (float)fabs(v));
+            double span;
+            h = sr_half(v * sc, dither32(kDitherX, (uint64_t)row, (uint32_t)k, __float_as_uint(xf)), &span);
+            span = ldexp(span, -xexp);
+            u2 += span * span;
+            uinf = fmaxf(uinf, (float)span);
         }
-        const __half h = __double2half(v * sc);
         const double hd = (double)__half2float(h);
         o[k] = h;
         o8[k] = to_e4m3(hd * (1.0 / 32.0));
@@ -130,14 +211,20 @@ __global__ void data_pack_f8_kernel(const float *__restrict__ X, int64_t n, int 
     }
     nrm = warp_sum(nrm);
     sq = warp_sum(sq);
+    u2 = warp_sum(u2);
+    xinf = warp_max(xinf);
+    uinf = warp_max(uinf);
     if (lane == 0) {
-        xnorm[row] = (float)sqrt(nrm);
+        const float xn = (float)sqrt(nrm);
+        xnorm[row] = xn;
         x2[row] = sq;
+        if (xstat) xstat[row] = make_float4(xn, xinf, uinf, (float)sqrt(u2));
     }
 }
 
 // ------------------------------------------------------------- codebook prep
-// ws layout: mu f32[d] | mu_nu f64[d] | stats f32[4] {nmax, dabsmax, -, -}
+// ws layout: mu f32[d] | mu_nu f64[d] | nrm f32[K] | stats f32[8] {max|delta_j|,
+// max|delta_jk|, max|c_j|, max|ulp(delta_j)|_2, max ulp(delta_jk), -, -, -}
 __global__ void cb_colmean(const float *__restrict__ W, int K, int d, const float *__restrict__ nu,
                            float *__restrict__ mu, double *__restrict__ mu_nu) {
     // one warp per column: lane-strided partial sums then a fixed xor tree
@@ -163,8 +250,8 @@ __global__ void cb_rowstats(const float *__restrict__ W, int K, int d, const flo
     if (j >= K) return;
     const float *w = W + (int64_t)j * d;
     const float *w0 = W;
-    double n2 = 0.0, cm = 0.0, sq = 0.0;
-    float amax = 0.0f;
+    double n2 = 0.0, cm = 0.0, sq = 0.0, u2 = 0.0;
+    float amax = 0.0f, uinf = 0.0f;
     bool same0 = j > 0;
     for (int k = lane; k < d; k += 32) {
         float wf = w[k];
@@ -175,11 +262,25 @@ __global__ void cb_rowstats(const float *__restrict__ W, int K, int d, const flo
         cm += mu_nu[k] * dl;
         sq += wv * wv;
         amax = fmaxf(amax, (float)fabs(dl));
+        // error span of the stochastic fp16 rounding of dl (cb_pack): the
+        // fp16 grid is scale-invariant for powers of two, so the span of the
+        // scaled value is this one times 2^sexp (normal range; the
+        // subnormal floor is added in cb_pack)
+        const double a = fabs(dl);
+        if (a > 0.0) {
+            const double sp = ldexp(1.0, ilogb(a) - 10);
+            if (a / sp != floor(a / sp)) {
+                u2 += sp * sp;
+                uinf = fmaxf(uinf, (float)sp);
+            }
+        }
     }
     n2 = warp_sum(n2);
     cm = warp_sum(cm);
     sq = warp_sum(sq);
+    u2 = warp_sum(u2);
     amax = warp_max(amax);
+    uinf = warp_max(uinf);
     // A node bit-identical to node 0 ties it exactly in every distance, and
     // ties resolve to the lowest index (kernels.py:27-28): mask it out of the
     // screen (c = +inf).  Covers the collapsed maps of SURVEY.md A.8.
@@ -193,6 +294,8 @@ __global__ void cb_rowstats(const float *__restrict__ W, int K, int d, const flo
         nrm_out[j] = nr;
         atomic_max_nonneg(&stats[0], nr);
         atomic_max_nonneg(&stats[1], amax);
+        atomic_max_nonneg(&stats[3], (float)sqrt(u2));
+        atomic_max_nonneg(&stats[4], uinf);
     }
 }
 
@@ -205,7 +308,11 @@ __device__ __forceinline__ int pick_exp(float amax, int top = 14) {
     return top - e;
 }
 
-// W8 (2-pass mode, Wl unused): [e4m3(wl * 32) | e4m3(wh / 32)], 2 dp bytes per row
+// Wh = fp16(delta 2^sexp): stochastic rounding (dither from (node, feature,
+// value bits), so a new codebook draws fresh dither) unless Wl is given (the
+// 3-pass screen: round-to-nearest hi + fp16 residual Wl).
+// W8 (2-pass mode, Wl unused): [e4m3(wl * 32) | e4m3(wh / 32)], 2 dp bytes
+// per row, wl = the residual of the (stochastic) hi.
 __global__ void cb_pack(const float *__restrict__ W, int K, int d, const float *__restrict__ mu,
                         int xexp, __half *__restrict__ Wh, __half *__restrict__ Wl, int dp, int kp,
                         float *__restrict__ c, const float *__restrict__ stats,
@@ -214,44 +321,47 @@ __global__ void cb_pack(const float *__restrict__ W, int K, int d, const float *
     int lane = threadIdx.x & 31;
     if (j >= kp) return;
     int sexp = pick_exp(stats[1], W8 ? 13 : 14);
-    if (W8) {
-        uint8_t *o8 = W8 + (int64_t)j * (2 * dp);
+    __half *o = Wh ? Wh + (int64_t)j * dp : nullptr;
+    __half *ol = Wl ? Wl + (int64_t)j * dp : nullptr;
+    uint8_t *o8 = W8 ? W8 + (int64_t)j * (2 * dp) : nullptr;
+    if (o == nullptr) {
+        if (j >= K && lane == 0) c[j] = INFINITY;
+    } else {
         const float *w = W + (int64_t)(j < K ? j : 0) * d;
         const double sc = ldexp(1.0, sexp);
         for (int k = lane; k < dp; k += 32) {
-            const double v = (j < K && k < d) ? ((double)w[k] - (double)mu[k]) * sc : 0.0;
-            const double hd = (double)__half2float(__double2half(v));
-            o8[k] = to_e4m3((v - hd) * 32.0);
-            o8[dp + k] = to_e4m3(hd * (1.0 / 32.0));
-        }
-    }
-    __half *o = Wh ? Wh + (int64_t)j * dp : nullptr;
-    __half *ol = Wl ? Wl + (int64_t)j * dp : nullptr;
-    if (o == nullptr) {
-        if (j >= K && lane == 0) c[j] = INFINITY;
-    } else if (j < K) {
-        const float *w = W + (int64_t)j * d;
-        double sc = ldexp(1.0, sexp);
-        for (int k = lane; k < dp; k += 32) {
-            double v = k < d ? ((double)w[k] - (double)mu[k]) * sc : 0.0;
-            __half h = __double2half(v);
+            const bool live = j < K && k < d;
+            const float wf = live ? w[k] : 0.0f;
+            const double v = live ? ((double)wf - (double)mu[k]) * sc : 0.0;
+            __half h;
+            if (ol) {
+                h = __double2half(v);
+                ol[k] = __double2half(v - (double)__half2float(h));
+            } else {
+                double span;
+                h = sr_half(v, dither32(kDitherW, (uint64_t)j, (uint32_t)k, __float_as_uint(wf)), &span);
+            }
             o[k] = h;
-            if (ol) ol[k] = __double2half(v - (double)__half2float(h));
+            if (o8) {
+                const double hd = (double)__half2float(h);
+                o8[k] = to_e4m3((v - hd) * 32.0);
+                o8[dp + k] = to_e4m3(hd * (1.0 / 32.0));
+            }
         }
-    } else {
-        for (int k = lane; k < dp; k += 32) {
-            o[k] = __double2half(0.0);
-            if (ol) ol[k] = __double2half(0.0);
-        }
-        if (lane == 0) c[j] = INFINITY;
+        if (j >= K && lane == 0) c[j] = INFINITY;
     }
     if (j == 0 && lane == 0) {
         // r = c_j - 2 * (x' . delta): acc * 2^-(xexp + sexp) is the dot product
         scal[0] = -2.0f * ldexpf(1.0f, -(xexp + sexp));
         scal[1] = stats[0];     // max_j |delta_j|
         scal[2] = (float)sexp;
-        scal[3] = stats[1];
-        scal[4] = stats[2];     // max_j |c_j| (fp32 rounding slack of the sparse window)
+        scal[3] = stats[1];     // max_jk |delta_jk|
+        scal[4] = stats[2];     // max_j |c_j| (fp32 rounding slack of the windows)
+        // max_j |ulp(delta_j)|_2 and max_jk ulp(delta_jk) of the stochastic
+        // rounding, plus the subnormal floor (spacing 2^-24 after scaling)
+        const float floor_sp = ldexpf(1.0f, -24 - sexp);
+        scal[5] = stats[3] + floor_sp * sqrtf((float)dp);
+        scal[6] = fmaxf(stats[4], floor_sp);
     }
 }
 
@@ -281,13 +391,14 @@ extern "C" int somb_data_stats(const float *X, int64_t n, int32_t d, float *nu, 
 }
 
 extern "C" int somb_data_pack(const float *X, int64_t n, int32_t d, const float *nu, int32_t xexp,
-                              uint16_t *Xh, uint16_t *Xl, int32_t dp, float *xnorm, double *x2, void *stream) {
+                              uint16_t *Xh, uint16_t *Xl, int32_t dp, float *xnorm, double *x2, float *xstat,
+                              void *stream) {
     SOMB_REQUIRE(d > 0 && dp >= d && dp % 8 == 0, SOMB_E_INPUT, "data_pack: bad pitch d=%d dp=%d", d, dp);
     if (n == 0) return SOMB_OK;
     int rows_per_block = 8;
     int64_t blocks = (n + rows_per_block - 1) / rows_per_block;
     data_pack_kernel<<<(unsigned)blocks, 32 * rows_per_block, 0, as_stream(stream)>>>(
-        X, n, d, nu, xexp, (__half *)Xh, (__half *)Xl, dp, xnorm, x2);
+        X, n, d, nu, xexp, (__half *)Xh, (__half *)Xl, dp, xnorm, x2, reinterpret_cast<float4 *>(xstat));
     note_launch();
     SOMB_LAUNCH_CHECK("somb_data_pack");
     return SOMB_OK;
@@ -309,7 +420,7 @@ extern "C" int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const
     double *mu_nu = (double *)p;       p += align_up((size_t)d * sizeof(double), 256);
     float *nrm = (float *)p;           p += align_up((size_t)K * sizeof(float), 256);
     float *stats = (float *)p;
-    cudaMemsetAsync(stats, 0, 4 * sizeof(float), st);
+    cudaMemsetAsync(stats, 0, 8 * sizeof(float), st);
     cb_colmean<<<(d + 7) / 8, 256, 0, st>>>(W, K, d, nu, mu, mu_nu);
     note_launch();
     cb_rowstats<<<(K + 7) / 8, 256, 0, st>>>(W, K, d, mu, mu_nu, c, w2, nrm, stats);
@@ -323,13 +434,13 @@ extern "C" int somb_codebook_prepare(const float *W, int32_t K, int32_t d, const
 }
 
 extern "C" int somb_data_pack_f8(const float *X, int64_t n, int32_t d, const float *nu, int32_t xexp, uint16_t *Xh,
-                                 uint8_t *X8, int32_t dp, float *xnorm, double *x2, void *stream) {
+                                 uint8_t *X8, int32_t dp, float *xnorm, double *x2, float *xstat, void *stream) {
     SOMB_REQUIRE(d > 0 && dp >= d && dp % 8 == 0 && Xh && X8, SOMB_E_INPUT, "data_pack_f8: bad pitch d=%d dp=%d", d,
                  dp);
     if (n == 0) return SOMB_OK;
     int64_t blocks = (n + 7) / 8;
     data_pack_f8_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(X, n, d, nu, xexp, (__half *)Xh, X8, dp,
-                                                                         xnorm, x2);
+                                                                         xnorm, x2, reinterpret_cast<float4 *>(xstat));
     note_launch();
     SOMB_LAUNCH_CHECK("somb_data_pack_f8");
     return SOMB_OK;
@@ -346,7 +457,7 @@ extern "C" int somb_codebook_prepare_f8(const float *W, int32_t K, int32_t d, co
     double *mu_nu = (double *)p;       p += align_up((size_t)d * sizeof(double), 256);
     float *nrm = (float *)p;           p += align_up((size_t)K * sizeof(float), 256);
     float *stats = (float *)p;
-    cudaMemsetAsync(stats, 0, 4 * sizeof(float), st);
+    cudaMemsetAsync(stats, 0, 8 * sizeof(float), st);
     cb_colmean<<<(d + 7) / 8, 256, 0, st>>>(W, K, d, nu, mu, mu_nu);
     note_launch();
     cb_rowstats<<<(K + 7) / 8, 256, 0, st>>>(W, K, d, mu, mu_nu, c, w2, nrm, stats);

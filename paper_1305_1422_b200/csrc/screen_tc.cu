@@ -272,7 +272,7 @@ template <int CG, int PASSES, int HC, int MC = 1, int EPI = TC_EPI_WARPS>
 __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const CUtensorMap *map_w,
                                                const CUtensorMap *map_xl, const CUtensorMap *map_wl, int64_t n,
                                                int dp, int kp, const float *__restrict__ c,
-                                               const float *__restrict__ xnorm, const float *__restrict__ scal,
+                                               const float *__restrict__ xstat, const float *__restrict__ scal,
                                                float wcoef, const float *__restrict__ thr0, int *__restrict__ cand,
                                                int *__restrict__ ccount, int *__restrict__ flags,
                                                float *__restrict__ dump, unsigned *__restrict__ sync_ctr,
@@ -482,7 +482,6 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
         const int et = ew * 32 + lane;         // buffer slot owner id
         constexpr int GS = SOMB_CAND_CAP / Cfg::NGRP;   // candidate slots per group
         const float m = scal[0];
-        const float nmax = scal[1];
         const CandBuf cb{smem_u32(cbv + et), smem_u32(cbi + et), 4u * EPI * 32};
         int acc = 0;
         uint32_t aphase = 0;
@@ -492,7 +491,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             const int64_t row = (int64_t)u * unit_rows + TC_ROWS * crank + quad * 32 + lane;
             const bool live = row < n;
             CandRow<Cfg::HALF_CAP> st;
-            cand_init(st, live ? wcoef * xnorm[row] * nmax : 0.0f);
+            cand_init(st, live ? wcoef * screen_sigma(reinterpret_cast<const float4 *>(xstat)[row], scal) : 0.0f);
             if (live && thr0) st.thr = thr0[row];
             const bool dumping = dump != nullptr && live;
             for (int nt = 0; nt < NT; ++nt) {
@@ -577,26 +576,26 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
 #define SCREEN_TC_ARGS                                                                                              \
     const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,                           \
         const __grid_constant__ CUtensorMap map_xl, const __grid_constant__ CUtensorMap map_wl, int64_t n, int dp, int kp, \
-        const float *__restrict__ c, const float *__restrict__ xnorm, const float *__restrict__ scal, float wcoef,  \
+        const float *__restrict__ c, const float *__restrict__ xstat, const float *__restrict__ scal, float wcoef,  \
         const float *__restrict__ thr0, int *__restrict__ cand, int *__restrict__ ccount, int *__restrict__ flags,  \
         float *__restrict__ dump, unsigned *__restrict__ sync_ctr, int lag, OvfPool pool, int *__restrict__ ovf_head, \
         float *__restrict__ ovf_lim
 
 template <int P, int HC>
 __global__ void __launch_bounds__(TC_THREADS, 1) screen_tc1_kernel(SCREEN_TC_ARGS) {
-    screen_tc_body<1, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
+    screen_tc_body<1, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xstat, scal, wcoef, thr0, cand, ccount,
                              flags, dump, sync_ctr, lag, pool, ovf_head, ovf_lim);
 }
 
 template <int P, int HC>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1) screen_tc4_kernel(SCREEN_TC_ARGS) {
-    screen_tc_body<2, P, HC, 2>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
+    screen_tc_body<2, P, HC, 2>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xstat, scal, wcoef, thr0, cand, ccount,
                                 flags, dump, sync_ctr, lag, pool, ovf_head, ovf_lim);
 }
 
 template <int P, int HC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) screen_tc2_kernel(SCREEN_TC_ARGS) {
-    screen_tc_body<2, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xnorm, scal, wcoef, thr0, cand, ccount,
+    screen_tc_body<2, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xstat, scal, wcoef, thr0, cand, ccount,
                              flags, dump, sync_ctr, lag, pool, ovf_head, ovf_lim);
 }
 
@@ -696,7 +695,7 @@ int screen_tc_set_knob(const char *key, int value) {
 }
 
 int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, const __half *Wh, const __half *Wl, int kp,
-                     const float *c, const float *xnorm, const float *scal, float wcoef, const float *thr0, int *cand,
+                     const float *c, const float *xstat, const float *scal, float wcoef, const float *thr0, int *cand,
                      int *ccount, int *flags, float *dump, unsigned *ctrs, OvfPool pool, int *ovf_head,
                      float *ovf_lim, int passes, cudaStream_t st) {
     SOMB_REQUIRE(dp % 8 == 0 && kp % TC_BN == 0, SOMB_E_INPUT, "screen_tc: dp %% 8 and kp %% 256 required");
@@ -755,7 +754,7 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
     int grid = cg * (units < max_units ? units : max_units);
     if (mcv == 2) grid = 4 * ((grid + 3) / 4);
 #define SCREEN_LAUNCH(KERN, CGV, PV, HV)                                                                            \
-    KERN<PV, HV><<<grid, TC_THREADS, TcCfg<CGV, PV, HV>::SMEM, st>>>(mx, mw, mxl, mwl, n, dp, kp, c, xnorm, scal, wcoef, \
+    KERN<PV, HV><<<grid, TC_THREADS, TcCfg<CGV, PV, HV>::SMEM, st>>>(mx, mw, mxl, mwl, n, dp, kp, c, xstat, scal, wcoef, \
                                                                      thr0, cand, ccount, flags, dump, ctr, lag, pool, \
                                                                      ovf_head, ovf_lim)
     if (two) {

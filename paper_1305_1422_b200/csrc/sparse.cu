@@ -14,6 +14,8 @@
 
 namespace somb {
 
+int launch_repair_truncated(const int *flags, int *ccount, int64_t n, unsigned *ctrs, cudaStream_t st);
+
 constexpr int SP_WARPS = 8;
 constexpr int SP_NNZ_BUF = 256;      // staged (col, val) pairs per warp
 constexpr int SP_CAP = 32;           // candidates in shared memory per row before spilling to the pool
@@ -417,6 +419,8 @@ extern "C" int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const 
                 w.ovf_lim);
         }
         note_launch();
+        int rc = launch_repair_truncated(flags, ccount, n, w.ctrs, st);   // truncated rows -> exact full scan
+        if (rc) return rc;
     } else {
         cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
     }

@@ -26,11 +26,19 @@ from . import _lib, errors
 from .datasets import DenseDataset, SparseDataset, _is_torch
 from .grid import GridType, MapType, Neighborhood, distance_table
 
-_DEF_WINDOW_KAPPA = float(os.environ.get("SOMB_WINDOW_KAPPA", "10.0"))   # screening window = kappa * u16 * |x-nu| * max|delta| / sqrt(D); measured max screen error <= 6.1 units (tools/calib_screen.py): 1.6x margin; cfg2 1M x 10 epochs bit-identical to the exact scan at kappa 10 (profiles/)
+# Screening windows, in units of the per-row sigma_i of the stochastically
+# rounded fp16 operands (csrc/cand.cuh screen_sigma): the
+# window of row i is kappa * sigma_i.  Calibrated on hardware over uniform,
+# duplicated-column, near-constant, blob, one-hot, integer, offset and
+# low-rank data (tools/calib_screen.py, profiles/r2_window_calib_*.json).
+_DEF_WINDOW_KAPPA = float(os.environ.get("SOMB_WINDOW_KAPPA", "5.0"))     # 1-pass fp16
+_DEF_WINDOW_KAPPA2 = float(os.environ.get("SOMB_WINDOW_KAPPA2", "0.5"))   # fp16 + fp8 cross terms
 _U16 = 2.0 ** -11
-# 3-pass split screen (hi.hi + hi.lo + lo.hi): its error is dominated by fp32
-# accumulation, measured max ~ D/8192 in the same units (tools/calib_screen.py:
-# 0.01 / 0.03 / 0.09 at D = 128 / 256 / 1000); the window is 2.6x that + 0.02.
+# 3-pass split screen (hi.hi + hi.lo + lo.hi, round-to-nearest): its error is
+# dominated by fp32 accumulation, measured max ~ D/8192 in units of
+# 2^-11 |x'| max|delta| / sqrt(D) (tools/calib_screen.py: 0.01 / 0.03 / 0.09
+# at D = 128 / 256 / 1000); the window is 2.6x that + 0.02 (somb_data_pack
+# encodes that unit as the row's sigma for the 3-pass operands).
 def _kappa3(d: int) -> float:
     return 2.6 * d / 8192.0 + 0.02
 
@@ -43,12 +51,15 @@ class EngineOptions:
     seed_prev: bool = True            # seed the screen threshold from the previous BMUs
     screen_passes: int = 0            # 0 auto (2 if the padded feature count <= 256), 1, 2 (fp16 + fp8 cross terms) or 3
     window_kappa3: Optional[float] = None     # None: _kappa3(d)
-    window_kappa2: float = float(os.environ.get("SOMB_WINDOW_KAPPA2", "0.6"))   # 2-pass (fp16 + fp8) window: measured max error ~0.22 units (tools/f8_probe.py)
+    window_kappa2: float = _DEF_WINDOW_KAPPA2   # 2-pass (fp16 + fp8 cross terms) window, sigma units
     conv: str = "auto"                # neighbourhood convolution: "auto", "direct", "spectral"
     rerank_order: bool = True         # re-rank rows in previous-BMU order (L2 locality; same result)
     shard_update: str = "columns"     # multi-rank update: "columns" (reduce-scatter S by feature columns,
                                       # each rank updates its columns for all nodes) or "nodes" (all-reduce S,
                                       # node-slice update, row all-gather)
+    exchange: str = os.environ.get("SOMB_EXCHANGE", "auto")   # "auto": collectives only when world > 1;
+                                      # "always": run the sharded exchange (NCCL) even in a 1-rank group
+                                      # (tests the NCCL data plane and times it on one GPU)
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -64,6 +75,7 @@ def _round_up(v: int, a: int) -> int:
 
 
 _STAGE = {}   # (device index, slot, thread) -> two cached page-locked staging halves
+_STAGE_EVENTS = {}   # same key -> the events of the last copies that read each upload half
 
 
 def to_host(t: torch.Tensor, slot: str = "main") -> np.ndarray:
@@ -119,7 +131,10 @@ def to_device(a: np.ndarray, dev) -> torch.Tensor:
     src = a.reshape(-1).view(np.uint8)
     dst = out.view(-1).view(torch.uint8)
     stream = torch.cuda.current_stream(out.device)
-    events = [None, None]
+    # the last H2D of the previous call may still be reading a half: its
+    # events persist with the buffers (a back-to-back upload -- the CSR cols
+    # then vals -- must not overwrite a half that is still in flight)
+    events = _STAGE_EVENTS.setdefault(key, [None, None])
     for i, o in enumerate(range(0, nbytes, chunk)):
         b = bufs[i % 2]
         if events[i % 2] is not None:
@@ -165,6 +180,11 @@ def pick_device(device=None) -> torch.device:
     return torch.device("cuda", idx)
 
 
+def _dist_ready() -> bool:
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized()
+
+
 def dist_info(group=None):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
@@ -184,6 +204,9 @@ class SomEngine:
         self.opt = options or EngineOptions()
         self.group = group
         self.rank, self.world = dist_info(group)
+        # the per-epoch exchange runs when the rows are sharded, or on demand
+        # in a 1-rank process group (EngineOptions.exchange = "always")
+        self.sharded = self.world > 1 or (self.opt.exchange == "always" and _dist_ready())
         self.nx, self.ny = int(n_columns), int(n_rows)
         self.K = self.nx * self.ny
         self.map_type, self.grid = map_type, grid
@@ -266,7 +289,7 @@ class SomEngine:
             kappa = self.opt.window_kappa2
         else:
             kappa = self.opt.window_kappa
-        return float(kappa * _U16 / math.sqrt(self.d))
+        return float(kappa)
 
     # ------------------------------------------------------------ dataset
     def _upload_dense(self, x, dry=False):
@@ -300,8 +323,11 @@ class SomEngine:
             self.Xl = torch.empty((max(n, 1), 2 * self.dp), dtype=torch.uint8, device=dev)
         self.xnorm = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         self.x2 = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        # per-row window terms {|x'|, max|x'_k|, max ulp_k, |ulp|_2} (cand.cuh screen_sigma)
+        self.xstat = torch.empty((max(n, 1), 4), dtype=torch.float32, device=dev)
         _lib.call("somb_data_pack_f8" if passes == 2 else "somb_data_pack", _ptr(self.X), n, d, _ptr(self.nu),
-                  self.xexp, _ptr(self.Xh), _ptr(self.Xl), self.dp, _ptr(self.xnorm), _ptr(self.x2), st)
+                  self.xexp, _ptr(self.Xh), _ptr(self.Xl), self.dp, _ptr(self.xnorm), _ptr(self.x2),
+                  _ptr(self.xstat), st)
 
     # ----------------------------------------------------------- codebook
     def set_codebook(self, w):
@@ -373,7 +399,7 @@ class SomEngine:
         st = _stream(self.dev)
         self._mark("screen", True)
         prev = self.bmu if (self.has_prev and self.opt.seed_prev) else None
-        _lib.call("somb_bmu_screen", _ptr(self.Xh), _ptr(self.Xl), _ptr(self.xnorm), self.n, self.dp,
+        _lib.call("somb_bmu_screen", _ptr(self.Xh), _ptr(self.Xl), _ptr(self.xstat), self.n, self.dp,
                   _ptr(self.Wh), _ptr(self.Wl), _ptr(self.c), self.K, self.kp, _ptr(self.scal),
                   C.c_float(self.window_coef),
                   _ptr(prev), self.screen_impl, _ptr(self.flags), _ptr(self.ws), st)
@@ -391,7 +417,7 @@ class SomEngine:
         self.prepare()
         m = min(self.n, 128)
         dump = torch.full((m, self.kp), float("nan"), dtype=torch.float32, device=self.dev)
-        _lib.call("somb_debug_screen_dump", _ptr(self.Xh), _ptr(self.Xl), _ptr(self.xnorm), self.n,
+        _lib.call("somb_debug_screen_dump", _ptr(self.Xh), _ptr(self.Xl), _ptr(self.xstat), self.n,
                   self.dp, _ptr(self.Wh), _ptr(self.Wl), _ptr(self.c), self.kp, _ptr(self.scal),
                   C.c_float(self.window_coef), self.passes,
                   _ptr(dump), _ptr(self.ws), _stream(self.dev))
@@ -404,6 +430,11 @@ class SomEngine:
         if self.screen_impl in (0, 3):   # one count byte per column group (2 or 4 groups)
             return (cc & 255) + ((cc >> 8) & 255) + ((cc >> 16) & 255) + ((cc >> 24) & 255)
         return cc
+
+    def repaired_rows(self) -> int:
+        """Rows of the last screen whose truncated candidate set was replaced
+        by an exact scan of every node (host sync)."""
+        return int(_lib.load().somb_bmu_repaired_rows(_ptr(self.ws), self.n, _stream(self.dev)))
 
     def overflow_chunks(self) -> int:
         """Overflow chunks the last tcgen05 screen spilled (bmu.cu workspace counters)."""
@@ -432,7 +463,7 @@ class SomEngine:
             self._Wnew = torch.empty((K, dc), dtype=torch.float32, device=dev)
 
     def reduce(self):
-        if self.world > 1:
+        if self.sharded:
             from .parallel import allreduce_sum, reduce_scatter_columns
             if self.opt.shard_update == "columns":
                 # this rank's feature columns of S, summed over ranks; the
@@ -448,7 +479,7 @@ class SomEngine:
         hood = _lib.SombHood(_lib.NBH_BUBBLE if neighborhood is Neighborhood.BUBBLE
                              else _lib.NBH_GAUSSIAN, int(bool(compact)), float(radius), float(cutoff),
                              {"auto": 0, "direct": 1, "spectral": 2}[self.opt.conv], 0)
-        if self.world > 1 and not all_nodes and self.opt.shard_update == "columns":
+        if self.sharded and not all_nodes and self.opt.shard_update == "columns":
             # all nodes, this rank's columns: the update is independent per
             # feature column, so each column is computed exactly as on one GPU
             from .parallel import allgather_columns
@@ -466,7 +497,7 @@ class SomEngine:
         _lib.call("somb_hood_update", _ptr(self.S), _ptr(self.cnt), self.d, C.byref(self.cmap),
                   C.byref(hood), C.c_double(scale), _ptr(self.dist_tab), _ptr(self.W), nb, ne,
                   _ptr(self.W2), _ptr(num_out), _ptr(den_out), _ptr(self.ws), _stream(self.dev))
-        if self.world > 1 and not all_nodes:
+        if self.sharded and not all_nodes:
             from .parallel import allgather_rows
             allgather_rows(self.W2, self.kc, self.group)
         self.W, self.W2 = self.W2, self.W

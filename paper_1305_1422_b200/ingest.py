@@ -51,14 +51,34 @@ def _to_f32(tokens: list, lineno_of) -> np.ndarray:
 
 
 def _dense_body(rows: list, width: int, mismatch) -> DenseDataset:
-    """rows: [(lineno, tokens)] all of `width` tokens (checked here)."""
-    for lineno, toks in rows:
-        if len(toks) != width:
-            raise mismatch(f"line {lineno}: expected {width} values, got {len(toks)}")
-    flat = [t for _, toks in rows for t in toks]
-    linenos = [no for no, _ in rows]
-    vals = _to_f32(flat, lambda k: linenos[k // max(width, 1)])
-    return DenseDataset(vals.reshape(len(rows), width))
+    """rows: [(lineno, tokens)] that must all hold `width` tokens.  The
+    reference checks and converts row by row (fileio.py:150-165, 215-220,
+    _parse_row 130-139), so the error raised is the first in file order of
+    a width mismatch, a non-numeric token or a non-finite value (within a
+    row in that order).  Here the conversion is one bulk numpy call over the
+    rows before the first width mismatch, and the failing row is located
+    afterwards."""
+    n_ok = next((i for i, (_, toks) in enumerate(rows) if len(toks) != width), len(rows))
+    flat = [t for _, toks in rows[:n_ok] for t in toks]
+    try:
+        vals = np.array(flat, dtype=np.float32)
+        n_num = n_ok
+    except ValueError:   # rows before the first one holding a non-numeric token
+        k = next(k for k, t in enumerate(flat) if not _is_number(t))
+        n_num = k // max(width, 1)
+        vals = np.array(flat[: n_num * width], dtype=np.float32)
+    vals = vals.reshape(n_num, width)
+    fin = np.isfinite(vals).all(axis=1)
+    if not fin.all():
+        raise errors.NonNumericToken(f"line {rows[int(np.argmin(fin))][0]}: non-finite value")
+    if n_num < n_ok:
+        lineno, toks = rows[n_num]
+        bad = next((t for t in toks if not _is_number(t)), toks[0])
+        raise errors.NonNumericToken(f"line {lineno}: token {bad!r} is not a number")
+    if n_ok < len(rows):
+        lineno, toks = rows[n_ok]
+        raise mismatch(f"line {lineno}: expected {width} values, got {len(toks)}")
+    return DenseDataset(vals)
 
 
 def parse_dense(src) -> DenseDataset:

@@ -44,7 +44,7 @@ def allreduce_sum(buf, group=None) -> None:
     [S | cnt | qe] accumulators over all ranks (replaces the rank-ordered
     fold of distributed.py:502-512).  NCCL on GPUs, gloo in CPU tests."""
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
 
 
@@ -57,8 +57,6 @@ def allgather_rows(buf, rows_per_rank: int, group=None) -> None:
     if not (dist.is_available() and dist.is_initialized()):
         return
     world = dist.get_world_size(group)
-    if world == 1:
-        return
     rank = dist.get_rank(group)
     mine = buf[rank * rows_per_rank:(rank + 1) * rows_per_rank].contiguous()
     if dist.get_backend(group) == "nccl":
@@ -78,18 +76,21 @@ def column_blocks(d: int, p: int) -> list[tuple[int, int]]:
 def reduce_scatter_columns(S, dc: int, staging, out, group=None) -> None:
     """out [K, dc] <- sum over ranks of this rank's column block of S [K, d]
     (zero-padded to p*dc columns): S is restaged block-major into `staging`
-    [p, K, dc] so the blocks are contiguous, then reduce-scattered (NCCL; the
-    gloo backend, used by the CPU tests, has no reduce-scatter: all-reduce
-    and take the block)."""
+    [p, K, dc] (one strided copy of the whole blocks, one of the ragged last
+    block; only padding columns are zeroed) so the blocks are contiguous,
+    then reduce-scattered (NCCL; the gloo backend, used by the CPU tests,
+    has no reduce-scatter: all-reduce and take the block)."""
     import torch.distributed as dist
     p = staging.shape[0]
     K, d = S.shape
-    if p * dc > d:
-        staging.zero_()   # padding columns of the last block(s)
-    for r in range(p):
-        a, b = min(d, r * dc), min(d, (r + 1) * dc)
-        if b > a:
-            staging[r, :, : b - a].copy_(S[:, a:b])
+    full = min(p, d // dc)                     # complete column blocks
+    if full:
+        staging[:full].copy_(S[:, : full * dc].view(K, full, dc).permute(1, 0, 2))
+    if full < p:
+        staging[full:].zero_()
+        rem = d - full * dc
+        if rem:
+            staging[full, :, :rem].copy_(S[:, full * dc:])
     rank = dist.get_rank(group)
     if dist.get_backend(group) == "nccl":
         dist.reduce_scatter_tensor(out, staging, op=dist.ReduceOp.SUM, group=group)
@@ -109,7 +110,9 @@ def allgather_columns(mine, staging, W, d: int, group=None) -> None:
         parts = [torch.empty_like(mine) for _ in range(p)]
         dist.all_gather(parts, mine, group=group)
         staging.copy_(torch.stack(parts, 0))
-    for r in range(p):
-        a, b = min(d, r * dc), min(d, (r + 1) * dc)
-        if b > a:
-            W[:, a:b].copy_(staging[r, :, : b - a])
+    full = min(p, d // dc)
+    if full:
+        W[:, : full * dc].view(K, full, dc).copy_(staging[:full].permute(1, 0, 2))
+    rem = d - full * dc
+    if full < p and rem:
+        W[:, full * dc: d].copy_(staging[full, :, :rem])

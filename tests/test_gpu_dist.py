@@ -124,3 +124,52 @@ def test_cli_local_and_torchrun_two_ranks(tmp_path):
     assert (n1, m1) == (n2, m2) == (9, 7)
     assert np.max(np.abs(w1.astype(np.float64) - w2) / np.maximum(np.abs(w1), 1e-6)) <= 1e-4
     assert (tmp_path / "two.bm").read_text().count("\n") == 3001
+
+
+def _nccl_single_worker(rank, port, x, out_dir):
+    """One rank, NCCL: the sharded exchange forced on (exchange="always"), so
+    reduce_scatter_tensor / all_gather_into_tensor / all_reduce /
+    barrier(device_ids) run over NCCL on the GPU (the data plane the 8-GPU
+    run uses; distributed.py:492-514)."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        import paper_1305_1422_b200 as S
+        from paper_1305_1422_b200.engine import EngineOptions
+        assert dist.get_backend() == "nccl"
+        dist.barrier(device_ids=[0])
+        out = {}
+        for mode in ("columns", "nodes"):
+            for big in (False, True):
+                cb, bmus, u = S.train(S.DenseDataset(x), _cfg(S, S.Kernel.DENSE_BLOCKED, big), device="cuda:0",
+                                      options=EngineOptions(exchange="always", shard_update=mode))
+                out[f"{mode}{int(big)}_w"], out[f"{mode}{int(big)}_b"], out[f"{mode}{int(big)}_u"] = \
+                    cb.weights, bmus, u.heights
+        dist.barrier(device_ids=[0])
+        np.savez(os.path.join(out_dir, "nccl1.npz"), **out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+def test_nccl_single_rank_exchange_matches_local(tmp_path):
+    """The NCCL branches of the exchange (column reduce-scatter + all-gather,
+    node-slice all-reduce + row all-gather) on hardware, in a 1-rank NCCL
+    group: the result must equal the local run bit for bit (with one rank
+    the collectives are identities, the column update is the same
+    arithmetic per column)."""
+    import torch.multiprocessing as mp
+    import paper_1305_1422_b200 as S
+    rng = np.random.default_rng(9)
+    centers = rng.random((10, 47)).astype(np.float32)
+    x = (centers[rng.integers(0, 10, 5000)] + 0.05 * rng.standard_normal((5000, 47))).astype(np.float32)
+    mp.spawn(_nccl_single_worker, args=(_free_port(), x, str(tmp_path)), nprocs=1, join=True)
+    got = np.load(tmp_path / "nccl1.npz")
+    for big in (False, True):
+        cb, bmus, u = S.train(S.DenseDataset(x), _cfg(S, S.Kernel.DENSE_BLOCKED, big), device="cuda:0")
+        for mode in ("columns", "nodes"):
+            assert np.array_equal(got[f"{mode}{int(big)}_w"], cb.weights), (mode, big)
+            assert np.array_equal(got[f"{mode}{int(big)}_b"], bmus), (mode, big)
+            assert np.array_equal(got[f"{mode}{int(big)}_u"], u.heights), (mode, big)

@@ -368,7 +368,7 @@ def test_bmu_search_one_call_matches_phases():
     ref_b, ref_d = eng.bmu[: eng.n].clone(), eng.d2min[: eng.n].clone()
     bmu = torch.full_like(eng.bmu, -1)
     d2 = torch.zeros_like(eng.d2min)
-    _lib.call("somb_bmu_search", _ptr(eng.Xh), _ptr(eng.Xl), _ptr(eng.X), _ptr(eng.xnorm), _ptr(eng.x2), eng.n,
+    _lib.call("somb_bmu_search", _ptr(eng.Xh), _ptr(eng.Xl), _ptr(eng.X), _ptr(eng.xstat), _ptr(eng.x2), eng.n,
               eng.d, eng.dp, _ptr(eng.Wh), _ptr(eng.Wl), _ptr(eng.W), _ptr(eng.c), _ptr(eng.w2), eng.K, eng.kp,
               _ptr(eng.scal), C.c_float(eng.window_coef), _ptr(ref_b), None, _lib.DIST_BLOCKED, 0,
               _ptr(bmu), _ptr(d2), _ptr(eng.flags), _ptr(eng.ws), _stream(eng.dev))

@@ -210,3 +210,79 @@ def test_native_writers_match_reference_format(tmp_path):
     fileio.write_bmus(bm, str(tmp_path / "a.bm"))
     ref = f"% {len(bm)}\n" + "".join(f"{i} {r} {c}\n" for i, (r, c) in enumerate(bm))
     assert (tmp_path / "a.bm").read_bytes() == ref.encode()
+
+
+def _hex_brute(c1, r1, c2, r2, nx, ny, toroid):
+    """Independent hex-lattice distance, the slow obvious way (modelled on the
+    reference's grid_distance_brute, tests/oracles.py:11-21): Cartesian node
+    positions (c + (r mod 2)/2, r sqrt(3)/2), on a torus the minimum over all
+    9 images of the (nx, ny sqrt(3)/2) period lattice."""
+    import math
+    x1, y1 = c1 + 0.5 * (r1 % 2), r1 * math.sqrt(3.0) / 2.0
+    x2, y2 = c2 + 0.5 * (r2 % 2), r2 * math.sqrt(3.0) / 2.0
+    shifts = (-1, 0, 1) if toroid else (0,)
+    return min(math.hypot(x1 - x2 + a * nx, y1 - y2 + b * ny * math.sqrt(3.0) / 2.0)
+               for a in shifts for b in shifts)
+
+
+@pytest.mark.parametrize("nx,ny", [(6, 4), (5, 6), (7, 2), (3, 8)])
+@pytest.mark.parametrize("mt", [S.MapType.PLANAR, S.MapType.TOROID])
+def test_hex_distance_vs_9_image_brute_force(nx, ny, mt):
+    """The hexagonal extension (package, oracle and -- through the GPU
+    update tests -- the device grid_d2) against the brute-force image sum,
+    every node pair; neighbours = the nodes at unit distance."""
+    tor = mt is S.MapType.TOROID
+    h = S.GridType.HEXAGONAL
+    d_or = O.distance_rows(np.arange(nx * ny), nx, ny, mt.value, O.HEX)
+    for a in range(nx * ny):
+        for b in range(nx * ny):
+            want = _hex_brute(a % nx, a // nx, b % nx, b // nx, nx, ny, tor)
+            got = S.grid_distance(S.GridCoord(a % nx, a // nx), S.GridCoord(b % nx, b // nx), mt, nx, ny, h)
+            assert got == pytest.approx(want, abs=1e-12), (a, b)
+            assert d_or[a, b] == pytest.approx(want, abs=1e-12), (a, b)
+        nb = {(c.row, c.col) for c in S.neighbors(S.GridCoord(a % nx, a // nx), mt, nx, ny, h)}
+        unit = {(b // nx, b % nx) for b in range(nx * ny) if b != a
+                and abs(_hex_brute(a % nx, a // nx, b % nx, b // nx, nx, ny, tor) - 1.0) < 1e-9}
+        assert nb == unit, (a, nb, unit)
+
+
+# Reference behaviour of the dense parsers on files with several defects
+# (first error in file order; within a row: width, non-numeric, non-finite),
+# recorded from somkit.fileio.parse_dense / parse_dense_headered
+# (fileio.py:130-220) in this container.
+@pytest.mark.parametrize("text,exc,msg", [
+    ("1 2\n3 x\n4 5 6\n", errors.NonNumericToken, "line 2: token 'x' is not a number"),
+    ("1 inf\n3 x\n", errors.NonNumericToken, "line 1: non-finite value"),
+    ("1 2\n3 4 5\nx y\n", errors.RowWidthMismatch, "line 2: expected 2 values, got 3"),
+    ("1 2\n1e39 0\n3\n", errors.NonNumericToken, "line 2: non-finite value"),
+    ("% 3\n% 2\n1 2\nq 1\n1 2 3\n", errors.NonNumericToken, "line 4: token 'q' is not a number"),
+    ("% 3\n% 2\n1 2\n1 2 3\nq 1\n", errors.HeaderBodyMismatch, "line 4: expected 2 values, got 3"),
+])
+def test_dense_error_order_matches_reference(text, exc, msg):
+    from paper_1305_1422_b200 import ingest
+    parse = ingest.parse_dense_headered if text.startswith("%") else ingest.parse_dense
+    with pytest.raises(exc) as ei:
+        parse(text)
+    assert str(ei.value) == msg
+
+
+def test_root_exports_reference_io_names():
+    # reference __init__.py:13-15 / __all__
+    for name in ("read_dataset", "detect_format", "parse_dense", "parse_dense_headered", "parse_sparse",
+                 "write_codebook", "write_bmus", "write_umatrix", "snapshot_paths"):
+        assert callable(getattr(S, name)) and name in S.__all__
+
+
+def test_bindings_sparse_branch_validation(tmp_path):
+    # bindings/__init__.py:91-98: kernel_type 2 reads a sparse file; a dense
+    # file is InvalidConfig, a wrong n_vectors is ShapeError (before compute)
+    from paper_1305_1422_b200 import bindings as B
+    sp = tmp_path / "x.sparse"
+    sp.write_text("0:1 2:0.5\n1:2\n")
+    dn = tmp_path / "x.dense"
+    dn.write_text("1 2 3\n4 5 6\n")
+    cb, bm, um = np.zeros(6 * 3, np.float32), np.zeros(4, np.int32), np.zeros(6, np.float32)
+    with pytest.raises(errors.InvalidConfig):
+        B.train_wrapper(str(dn), 1, 3, 2, 3, 2, 0, 0, "linear", 0, 0, "linear", 0, 2, "planar", "", cb, bm, um)
+    with pytest.raises(B.ShapeError):
+        B.train_wrapper(str(sp), 1, 3, 2, 3, 3, 0, 0, "linear", 0, 0, "linear", 0, 2, "planar", "", cb, bm, um)

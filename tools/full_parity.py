@@ -2,7 +2,8 @@
 the tcgen05 screen vs the exact fp64 scan (screen='exact'), same data, same
 initial codebook.  Reports codebook / U-matrix max relative error and the
 final BMU mismatches with their fp64 top-2 gaps.
-   python tools/full_parity.py [cfg] [rows] [epochs]"""
+   python tools/full_parity.py [cfg] [rows] [epochs] [family]
+family (dense configs): uniform (default) or a tools/calib_window.py family."""
 import json
 import os
 import sys
@@ -12,6 +13,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import bench  # noqa: E402
 import paper_1305_1422_b200 as S  # noqa: E402
 from paper_1305_1422_b200.engine import EngineOptions  # noqa: E402
@@ -26,9 +28,9 @@ if sparse:   # CSR rows of the bench generator; the screened search is the spars
     data = S.SparseDataset(d, rp.cpu().numpy(), cl.cpu().numpy(), vl.cpu().numpy())
     X = None
 else:
-    g = torch.Generator(device="cuda")
-    g.manual_seed(1001)
-    X = torch.rand((n, d), generator=g, device="cuda")
+    from calib_window import family_data
+    fam = sys.argv[4] if len(sys.argv) > 4 else "uniform"
+    X = family_data(fam, n, d, torch.device("cuda", 0))
     data = S.DenseDataset(X)
 cfg = S.TrainConfig(n_epochs=E, n_columns=nx, n_rows=ny, map_type=S.MapType(mt), grid=S.GridType(grid),
                     neighborhood=S.Neighborhood(nbh), compact_support=compact,
@@ -52,9 +54,10 @@ if len(bad) and not sparse:
     d2 = (xs * xs).sum(1, keepdim=True) + (W * W).sum(1)[None] - 2 * xs @ W.T
     t2 = torch.topk(d2, 2, dim=1, largest=False).values
     gap = float(((t2[:, 1] - t2[:, 0]) / t2[:, 0]).max())
-res = {"config": desc, "rows": n, "epochs": E, "codebook_max_rel": rel(wt, we),
+res = {"config": desc, "family": "sparse" if sparse else fam, "rows": n, "epochs": E,
+       "seconds_tensor": out["tensor"][3], "seconds_exact": out["exact"][3], "codebook_max_rel": rel(wt, we),
        "codebook_bit_identical_frac": float(np.mean(wt == we)), "umatrix_max_rel": rel(ut, ue),
        "bmu_mismatch": int(len(bad)), "bmu_mismatch_max_gap": gap}
 print(json.dumps(res))
 os.makedirs("gpurun_out", exist_ok=True)
-json.dump(res, open(f"gpurun_out/full_parity_{cfg_name}_{n}.json", "w"))
+json.dump(res, open(f"gpurun_out/full_parity_{cfg_name}_{res['family']}_{n}.json", "w"))
