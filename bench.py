@@ -155,6 +155,33 @@ def sparse_rows_device(n, d, nnz, seed, dev):
     return rowptr, cols.reshape(-1), vals.reshape(-1)
 
 
+def reference_rows(first, count, d, seed=1001):
+    """Rows [first, first + count) of the reference generator's dataset
+    gen_random_dense(n, d, seed) (reference bench.py:85-88, synth.py here):
+    numpy default_rng(seed).random((n, d), float32) consumes one 32-bit half
+    of a PCG64 output per value, so a rank's slice starts after advancing the
+    bit generator first*d/2 outputs (bit-identical to slicing the full array)."""
+    import numpy as np
+    skip = first * d
+    bg = np.random.PCG64(seed)
+    bg.advance(skip // 2)
+    g = np.random.Generator(bg)
+    if skip % 2:
+        g.random(1, dtype=np.float32)
+    return g.random((count, d), dtype=np.float32)
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return None
+
+
 def cpu_reference_rate(cfg_name, n_sub, steps, warmup, seed=1001):
     """Oracle port (numpy restatement of the reference path, kernels.py:365-450)
     on all host cores: search_accumulate(DENSE_BLOCKED) over an n_sub-row
@@ -189,6 +216,7 @@ def cpu_reference_rate(cfg_name, n_sub, steps, warmup, seed=1001):
     sa, bl = statistics.median(t_sa[k]), statistics.median(t_bl[k])
     t_epoch = (n / n_sub) * sa + bl
     return {"value": n * nx * ny / t_epoch, "unit": UNIT, "cores": workers, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{n_sub} of {n} rows x {nx * ny} nodes x {d} dims: search_accumulate "
                       f"({'SPARSE' if kern == O.SPARSE else 'DENSE_BLOCKED'}, {workers} workers) {sa:.2f} s + blend {bl:.2f} s per step, "
                       f"median of {len(t_sa[k])}; epoch = N/n_sub * search + blend",
@@ -235,10 +263,11 @@ def run_ours(args):
         eng = SparseEngine(sdata, nx, ny, mtype, gtype, device=dev, options=opts)
         X = None
     else:
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(1001 + rank)
-        X = torch.rand((count, d), generator=gen, device=dev, dtype=torch.float32)
-        eng = SomEngine(X, nx, ny, mtype, gtype, device=dev, options=opts)
+        # the reference generator's dataset (gen_random_dense(n, d, 1001)), this
+        # rank's contiguous row partition, uploaded from pageable numpy
+        Xnp = reference_rows(first, count, d)
+        eng = SomEngine(S.DenseDataset(Xnp), nx, ny, mtype, gtype, device=dev, options=opts)
+        X = None
     w0 = S.init_codebook(S.TrainConfig(n_columns=nx, n_rows=ny, seed=1), d).weights
     eng.set_codebook(w0)
     lib = _lib.load()
@@ -359,14 +388,10 @@ def run_ours(args):
     # end to end through the public API: host (pinned) data -> train() -> host results
     e2e = None
     if not args.no_e2e:
-        if sparse:
-            data = sdata
-        else:
-            Xh = torch.empty((count, d), dtype=torch.float32, pin_memory=True)
-            Xh.copy_(X)
-            data = S.DenseDataset(Xh)
+        # the drop-in input type: a DenseDataset over a pageable numpy array
+        # (or the SparseDataset of numpy CSR arrays), as a reference user passes it
+        data = sdata if sparse else S.DenseDataset(Xnp)
         del eng
-        X = None
         torch.cuda.empty_cache()
         kern = S.Kernel.SPARSE if sparse else S.Kernel.DENSE_BLOCKED
         cfg = S.TrainConfig(n_epochs=args.e2e_epochs, n_columns=nx, n_rows=ny, map_type=mtype,
@@ -388,14 +413,14 @@ def run_ours(args):
         e2e = {"value": n * K * args.e2e_epochs / te, "unit": UNIT,
                "h2d_bytes_per_step": int(count * SPARSE_NNZ * 8 + (count + 1) * 8 if sparse else count * d * 4),
                "d2h_bytes_per_step": int(K * d * 4 + n * 2 * 4 + K * 4),
-               "step": f"one public train() call: H2D of the rank's rows from pinned memory, seeded "
+               "step": f"one public train() call: H2D of the rank's rows from a pageable numpy array, seeded "
                        f"codebook init (on device, numpy-identical), {args.e2e_epochs} epochs, final naive "
                        f"BMU pass, U-matrix, D2H of codebook + BMU table + U-matrix",
                "seconds": te}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_rate(args.config, args.ref_rows, 1, 0)
+        cpu = cpu_reference_rate(args.config, args.ref_rows, 3, 1)
         cpu.pop("seconds_per_step", None)
 
     if rank == 0:
@@ -405,8 +430,10 @@ def run_ours(args):
                 "dtype": ("fp32 gather screen + f64 exact re-rank/update" if sparse else
                           {1: "fp16", 2: "fp16 + fp8 split", 3: "fp16 three-pass split"}.get(passes, "fp16")
                           + " tensor-core screen (fp32 accumulate) + f64 exact re-rank/update"),
-                "data": "synthetic uniform [0,1) fp32 (torch.Generator seed 1001+rank), codebook "
-                        "init default_rng(1)",
+                "data": ("synthetic text-like CSR (torch.Generator seed 1001+rank), codebook init default_rng(1)"
+                         if sparse else "synthetic uniform [0,1) fp32: the reference generator "
+                         "gen_random_dense(n, d, seed=1001) (numpy PCG64), rank r its partition rows; codebook "
+                         "init default_rng(1)"),
                 "config": {"workload": desc, "rows": n, "K": K, "d": d,
                            "schedule": f"{N_EPOCHS}-epoch linear radius {max(min(nx, ny) / 2, 1)}->1, "
                                        f"scale 1->0.01; step s = epoch s mod {N_EPOCHS}",
