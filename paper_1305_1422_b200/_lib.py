@@ -14,6 +14,9 @@ from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsomb200.so")
+# A/B measurement only (tools/ab.sh): load another build of the same library
+if os.environ.get("SOMB_LIB_PATH"):
+    LIB_PATH = os.environ["SOMB_LIB_PATH"]
 
 SOMB_OK, SOMB_E_CONFIG, SOMB_E_INPUT, SOMB_E_CUDA, SOMB_E_ARCH = 0, 1, 2, 3, 4
 GRID_RECT, GRID_HEX = 0, 1

@@ -7,7 +7,7 @@
 // whenever it lies in the screened candidate set.
 #include <cuda_fp8.h>
 
-#include "cand.cuh"
+#include "rerank.cuh"
 
 namespace somb {
 
@@ -24,8 +24,12 @@ static unsigned ovf_chunks(int64_t n) { return (unsigned)(4 * n > 4096 ? 4 * n :
 // test knob (somb_set_knob "ovf_chunks"): cap the usable overflow chunks to
 // exercise the pool-exhaustion path (0 = the whole pool)
 static unsigned g_ovf_limit = 0;
+// SOMB_RERANK_GROUP=0 / knob "rerank_group": per-row pipelined re-rank instead
+// of the grouped one (rerank_group.cu)
+static int g_rerank_group = -1;
 int bmu_set_knob(const char *key, int value) {
     if (!strcmp(key, "ovf_chunks")) { g_ovf_limit = value > 0 ? (unsigned)value : 0u; return SOMB_OK; }
+    if (!strcmp(key, "rerank_group")) { g_rerank_group = value < 0 ? -1 : value != 0; return SOMB_OK; }   // -1: default
     return SOMB_E_CONFIG;
 }
 
@@ -61,7 +65,7 @@ __global__ void repair_truncated_kernel(const int *__restrict__ flags, int *__re
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n) return;
     if (flags[row] & 0x01010101) {
-        ccount[row] = 0;
+        ccount[row] = kScanAll;
         atomicAdd(ctr, 1u);
     }
 }
@@ -75,43 +79,6 @@ int launch_repair_truncated(const int *flags, int *ccount, int64_t n, unsigned *
     return SOMB_OK;
 }
 
-// Spilled candidates of one row (tcgen05 screen overflow lists), read by the re-rank.
-struct OvfView {
-    const int *head;    // [4n] per (row, column group), nullptr = no overflow lists
-    const float *lim;   // [4n] final window limit of each column group
-    const int2 *ent;
-    const int *next, *cnt;
-    const unsigned *ngp;   // column groups of the tcgen05 lists (written by the screen)
-};
-
-// Candidate list of a row: one segment (SIMT screen) or NG column-group
-// segments (tcgen05 screen: count byte g, slots [g * 64 / NG, ...)).
-struct CandLayout {
-    int c[4];
-    int ng, gs, cnt;
-};
-__device__ __forceinline__ CandLayout cand_layout(int cc, int split, int ng) {
-    CandLayout L;
-    if (!split) {
-        L.ng = 1; L.gs = SOMB_CAND_CAP; L.c[0] = cc; L.c[1] = L.c[2] = L.c[3] = 0; L.cnt = cc;
-        return L;
-    }
-    L.ng = ng; L.gs = SOMB_CAND_CAP / ng; L.cnt = 0;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-        L.c[g] = g < ng ? (cc >> (8 * g)) & 255 : 0;
-        L.cnt += L.c[g];
-    }
-    return L;
-}
-__device__ __forceinline__ int cand_slot(const CandLayout &L, int q) {
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-        if (q < L.c[g]) return g * L.gs + q;
-        q -= L.c[g];
-    }
-    return 0;
-}
 
 // Seed of each row's acceptance threshold from its previous BMU: the screened
 // value of that node (same fp16 operands, fp32 FMA) plus one window and an
@@ -273,7 +240,7 @@ __global__ void rerank_kernel(const float *__restrict__ X, const double *__restr
     int cc = all ? 0 : ccount[row];
     const CandLayout L = cand_layout(cc, split, split && ov.ngp ? (int)*ov.ngp : 2);
     int cnt = L.cnt;
-    bool scan_all = all || cnt <= 0;
+    bool scan_all = all || cand_scan_all(L, ov, row);
     if (scan_all) cnt = K;
     double best = INFINITY;
     int bestj = 0x7fffffff;
@@ -390,7 +357,7 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
         int a = __shfl_sync(0xffffffffu, myj0, q & 31), b = __shfl_sync(0xffffffffu, myj1, q & 31);
         return q < 32 ? a : b;
     };
-    const bool all = cnt <= 0;       // safety net: exact scan of every node
+    const bool all = cand_scan_all(L, ov, row);   // repaired row: exact scan of every node
     if (all) cnt = K;
     const double xx = x2[row];
     double best = INFINITY;
@@ -457,25 +424,7 @@ rerank_vec_kernel(const float *__restrict__ X, const double *__restrict__ x2, in
 constexpr int RS = 4;            // candidate rows in flight per warp
 constexpr int RP_WARPS = 4;      // warps per block
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// fp32 -> fp64 without the XU pipe: the fp32 bit pattern re-read as an fp64
-// with the same exponent field is exactly w * 2^-896 (normal, subnormal and
-// zero alike); the 2^896 goes into the other operand, so every product and
-// difference below is bit-identical to the (double)w form.  3 ALU ops + 1
-// shift instead of one F2F.F64.F32, which issues at 1/8 warp-rate (it was the
-// busiest pipe of the re-rank; profiles/).  Inf / NaN codebook entries are not
-// preserved (they are finite garbage here, as anywhere after such an update).
-__device__ __forceinline__ double f32_as_f64_scaled(float v) {
-    const unsigned u = __float_as_uint(v);
-    return __hiloint2double((int)(((u & 0x7FFFFFFFu) >> 3) | (u & 0x80000000u)), (int)(u << 29));
-}
-constexpr double kF64Scale = 0x1p896;
 
 // Row operand of the pipelined re-rank: slices q < PQA convert w with F2F,
 // the rest with f32_as_f64_scaled (blocked mode keeps those x slices
@@ -570,7 +519,7 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
     auto slot = [&](int q) { return cand_slot(L, q); };
     const int myj0 = lane < cnt ? cand[row * SOMB_CAND_CAP + slot(lane)] : -1;
     const int myj1 = lane + 32 < cnt ? cand[row * SOMB_CAND_CAP + slot(lane + 32)] : -1;
-    const bool all = cnt <= 0;       // safety net: exact scan of every node
+    const bool all = cand_scan_all(L, ov, row);   // repaired row: exact scan of every node
     if (all) cnt = K;
     auto cand_at = [&](int q) {
         if (all) return q;
@@ -793,6 +742,12 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
     return launch_repair_truncated(flags, ccount, n, w.ctrs, st);
 }
 
+namespace somb {
+int launch_rerank_group(cudaStream_t st, const float *X, const double *x2, int64_t n, int d, const float *W,
+                        const double *w2, int K, const int *cand, const int *ccount, int mode, int split,
+                        const int *order, OvfView ov, int *bmu, double *d2min);
+}
+
 static int g_rerank_pipe = -1;   // SOMB_RERANK_PIPE=0 selects the unpipelined kernel (A/B testing)
 
 extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int32_t d, const float *W,
@@ -816,6 +771,14 @@ extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int3
     if (all) cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
     const int wpb = 8;
     const unsigned blocks = (unsigned)((n + wpb - 1) / wpb);
+    if (g_rerank_group < 0) {
+        const char *e = getenv("SOMB_RERANK_GROUP");
+        g_rerank_group = e ? atoi(e) != 0 : 0;
+    }
+    if (!all && d % 4 == 0 && g_rerank_group) {
+        return launch_rerank_group(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu,
+                                   d2min);
+    }
     if (!all && d % 4 == 0 && d <= 1024 && g_rerank_pipe) {
         if (d <= 128)
             launch_rerank_pipe<1>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);

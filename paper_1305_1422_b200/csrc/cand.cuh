@@ -145,8 +145,11 @@ __device__ __forceinline__ void cand_bound(CandRow<CAP> &s, float r_seen) {
     s.thr = fminf(s.thr, r_seen + s.win);
 }
 
+// (by value in, by value out: a reference would take the address of the
+// caller's CandRow and pin the whole row state to local memory for the
+// entire screen sweep -- an LDL of st.thr per chunk)
 template <int CAP, class Buf>
-__device__ __noinline__ void cand_make_room(CandRow<CAP> &s, Buf b, OvfPool pool) {
+__device__ __noinline__ CandRow<CAP> cand_make_room(CandRow<CAP> s, Buf b, OvfPool pool) {
     const float lim = s.rmin + s.win;
     int m = 0;
     for (int e = 0; e < s.cnt; ++e) {
@@ -158,7 +161,7 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, Buf b, OvfPool pool
         }
     }
     s.cnt = m;
-    if (m < CAP) return;
+    if (m < CAP) return s;
     // Full inside the window: spill the buffer into the overflow pool ...
     if (CAP <= kOvfChunk && pool.nchunks) {   // (buffers larger than a chunk never spill)
         const unsigned c = atomicAdd(pool.ctr, 1u);
@@ -170,7 +173,7 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, Buf b, OvfPool pool
             s.head = (int)c;
             s.cnt = 0;
             s.trunc |= 2;
-            return;
+            return s;
         }
     }
     // ... or, without room there, keep the 3 CAP / 4 smallest (value, index) pairs.
@@ -203,6 +206,7 @@ __device__ __noinline__ void cand_make_room(CandRow<CAP> &s, Buf b, OvfPool pool
     s.trunc |= 1;
     s.capbelow = fminf(s.capbelow, nextafterf(capv, -INFINITY));
     s.thr = fminf(s.thr, s.capbelow);
+    return s;
 }
 
 template <int CAP, class Buf>
@@ -213,7 +217,7 @@ __device__ __forceinline__ void cand_push(CandRow<CAP> &s, float r, int j, const
             s.rmin = r;
             s.thr = fminf(s.thr, r + s.win);
         }
-        if (s.cnt == CAP) cand_make_room<CAP>(s, b, pool);
+        if (s.cnt == CAP) s = cand_make_room<CAP>(s, b, pool);
         if (r <= s.thr) {
             cb_st(b, s.cnt, r, j);
             ++s.cnt;

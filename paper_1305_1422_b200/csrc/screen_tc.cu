@@ -67,10 +67,19 @@ struct TcCfg {
     static_assert(HC <= SOMB_CAND_CAP / 2, "column-group capacity exceeds the candidate list");
     static_assert(HC * NGRP <= SOMB_CAND_CAP, "candidate slots per row exceeded");
     static constexpr uint32_t CAND_BYTES = EPI * 32 * HALF_CAP * 8;
-    static constexpr int STAGES_RAW = (224 * 1024 - CAND_BYTES) / STAGE_BYTES;
+    // c_j of the tiles in flight: a ring of C_SLOTS 256-node slices (one per
+    // TMEM accumulator stage), bulk-copied by the producer, read by the
+    // epilogue as shared-memory broadcasts instead of L2 loads
+    static constexpr int C_SLOTS = 2;
+    static constexpr uint32_t C_BYTES = C_SLOTS * TC_BN * 4;
+    static constexpr uint32_t BAR_BYTES = 256;
+    // the dynamic shared window is 1024-byte aligned (declared __align__(1024),
+    // checked at kernel start), so the whole opt-in maximum is usable
+    static constexpr uint32_t SMEM_MAX = 232448;
+    static constexpr int STAGES_RAW = (int)((SMEM_MAX - CAND_BYTES - C_BYTES - BAR_BYTES) / STAGE_BYTES);
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static_assert(STAGES >= 2, "pipeline needs two stages");
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + CAND_BYTES + 1024 + 256;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + CAND_BYTES + C_BYTES + BAR_BYTES;
     // kind::f16 instruction descriptor: A,B = f16, D = f32, K-major, M = 128 CG, N = 256
     static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((128 * CG) >> 4) << 24);
 };
@@ -98,11 +107,23 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// arrive on the barrier at the same offset in cluster CTA `cta`
+// arrive on the barrier at the same offset in cluster CTA `cta`.  Default
+// (.release.cta) semantics: the arrive only has to order this thread's
+// tcgen05.ld reads (tcgen05.fence::before_thread_sync does that), not its
+// global stores -- the .release.cluster form compiled to MEMBAR.GPU + ERRBAR
+// per tile and warp, 14% of the cfg5 epilogue's stall samples
+// (profiles/r2_ncu_screen_cfg5_*.json).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar, uint32_t cta) {
     uint32_t remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(cta));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+// 1-D bulk copy global -> this CTA's shared memory, completing on `bar`
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
@@ -254,9 +275,10 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// 0 = normal; 1 = profiling mode (epilogue releases accumulators without
-// reading them: measures the TMA + tcgen05 feed alone).  Set from the
-// SOMB_SCREEN_PROFILE environment variable.
+// 0 = normal; profiling modes (SOMB_SCREEN_PROFILE or knob "screen_profile"):
+// 1 = the epilogue releases accumulators without reading them (the TMA +
+// tcgen05 feed alone), 2 = TMEM loads only, 3 = loads + window arithmetic
+// without the candidate path.
 __constant__ int g_profile_mode = 0;
 // 1 = load the data-row (A) tiles with an L2 evict_last policy (SOMB_A_EVICT_LAST, default 0: measured no gain at cfg2)
 __constant__ int g_a_evict_last = 0;
@@ -280,14 +302,18 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                                                float *__restrict__ ovf_lim) {
     using Cfg = TcCfg<CG, PASSES, HC, EPI>;
     constexpr int S = Cfg::STAGES;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw;
+    if (smem_u32(smem_raw) & 1023u) __trap();   // SWIZZLE_128B tiles need 1024-byte alignment
     // stage s: A_hi at smem + s*STAGE_BYTES, B_hi after it, then A_lo, B_lo (3-pass)
     float *cbv = (float *)(smem + S * Cfg::STAGE_BYTES);
     int *cbi = (int *)(cbv + EPI * 32 * Cfg::HALF_CAP);
-    uint64_t *bars = (uint64_t *)(smem + S * Cfg::STAGE_BYTES + Cfg::CAND_BYTES);
-    // bars: full[S] empty[S] tfull[2] tempty[2]; then the TMEM base address
-    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * S + 4);
+    float *cring = (float *)(smem + S * Cfg::STAGE_BYTES + Cfg::CAND_BYTES);
+    uint64_t *bars = (uint64_t *)(smem + S * Cfg::STAGE_BYTES + Cfg::CAND_BYTES + Cfg::C_BYTES);
+    // bars: full[S] empty[S] tfull[2] tempty[2] cfull[C_SLOTS] cempty[C_SLOTS]; then the TMEM base address
+    constexpr int CS = Cfg::C_SLOTS;
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * S + 4 + 2 * CS);
+    static_assert((2 * S + 4 + 2 * CS) * 8 + 4 <= (int)Cfg::BAR_BYTES, "barrier area");
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
     const uint32_t cl_rank = CG == 2 ? cluster_rank() : 0;
@@ -297,6 +323,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
     const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pair));
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t tfull0 = smem_u32(bars + 2 * S), tempty0 = smem_u32(bars + 2 * S + 2);
+    const uint32_t cfull0 = smem_u32(bars + 2 * S + 4), cempty0 = smem_u32(bars + 2 * S + 4 + CS);
 
     if (threadIdx.x == 0 && blockIdx.x == 0) sync_ctr[3] = Cfg::NGRP;   // candidate-list layout for the re-rank
     if (threadIdx.x == 0) {
@@ -307,6 +334,10 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull0 + 8 * a, 1);
             mbar_init(tempty0 + 8 * a, CG * EPI);   // one arrival per epilogue warp of the pair
+        }
+        for (int a = 0; a < CS; ++a) {
+            mbar_init(cfull0 + 8 * a, 1);           // the producer's expect_tx
+            mbar_init(cempty0 + 8 * a, EPI);        // one arrival per epilogue warp of this CTA
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map_x)) : "memory");
@@ -345,6 +376,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             const bool hint_a = g_a_evict_last != 0;
             int stage = 0;
             uint32_t phase = 0;
+            int cslot = 0;
+            uint32_t cphase = 0;
             // soft lockstep (lag > 0): a CTA starts its g-th node tile only once
             // all CTAs together have issued P * (g - lag) tiles, so concurrent
             // CTAs sweep the same codebook tiles and share them in L2
@@ -365,6 +398,14 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         }
                     }
                     const int node0 = nt * TC_BN + Cfg::B_ROWS * (int)crank;
+                    // c_j slice of this tile into ring slot `cslot` (once the
+                    // epilogue has finished the tile that used it before)
+                    auto load_c = [&]() {
+                        mbar_wait(cempty0 + 8 * cslot, cphase ^ 1);
+                        mbar_expect_tx(cfull0 + 8 * cslot, TC_BN * 4);
+                        bulk_load(smem_u32(cring + cslot * TC_BN), c + (size_t)nt * TC_BN, TC_BN * 4, cfull0 + 8 * cslot);
+                        if (++cslot == CS) { cslot = 0; cphase ^= 1; }
+                    };
                     for (int kb = 0; kb < KB8; ++kb) {   // PASSES == 2: fp8 cross terms first
                         mbar_wait(empty0 + 8 * stage, phase ^ 1);
                         const uint32_t fb = full0 + 8 * stage;
@@ -411,6 +452,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                             }
                         }
                         if (++stage == S) { stage = 0; phase ^= 1; }
+                        if (kb == KB - 1) load_c();   // issued with the tile's last stage: the slot is free by then
                     }
                     ++issued;
                     if (lag > 0) atomicAdd(sync_ctr, 1u);
@@ -485,6 +527,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
         const CandBuf cb{smem_u32(cbv + et), smem_u32(cbi + et), 4u * EPI * 32};
         int acc = 0;
         uint32_t aphase = 0;
+        int cslot = 0;
+        uint32_t cphase = 0;
         const int my_iters = MC == 1 ? (unit0 < num_units ? (num_units - unit0 + unit_step - 1) / unit_step : 0) : iters;
         for (int it = 0; it < my_iters; ++it) {
             const int u = unit0 + it * unit_step;
@@ -497,13 +541,17 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             for (int nt = 0; nt < NT; ++nt) {
                 mbar_wait(tfull0 + 8 * acc, aphase);
                 tc_fence_after();
+                mbar_wait(cfull0 + 8 * cslot, cphase);
+                const float *cs = cring + cslot * TC_BN;
                 if (g_profile_mode == 1) {   // profiling: release the accumulator untouched
                     __syncwarp();
                     if (lane == 0) {
                         if (CG == 1 || leader) mbar_arrive_local(tempty0 + 8 * acc);
                         else mbar_arrive_cluster(tempty0 + 8 * acc, cl_rank & ~1u);
+                        mbar_arrive_local(cempty0 + 8 * cslot);
                     }
                     if (++acc == 2) { acc = 0; aphase ^= 1; }
+                    if (++cslot == CS) { cslot = 0; cphase ^= 1; }
                     continue;
                 }
                 const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN);
@@ -511,12 +559,19 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                 for (int ch = half; ch < TC_BN / 32; ch += Cfg::NGRP) {
                     float v[32];
                     tmem_ld32(tbase + ch * 32, v);
+                    if (g_profile_mode == 2) {   // profiling: TMEM loads only
+                        float t = v[0];
+#pragma unroll
+                        for (int q = 1; q < 32; ++q) t = fminf(t, v[q]);
+                        if (__float_as_uint(t) == 0x7fc00001u) flags[0] = 1;   // never: keeps the loads
+                        continue;
+                    }
                     const int jc = nt * TC_BN + ch * 32;
-                    const float4 *cp = reinterpret_cast<const float4 *>(c + jc);
+                    const float4 *cp = reinterpret_cast<const float4 *>(cs + ch * 32);
                     float gmin[4];   // minima of the four 8-column groups
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        float4 cc = __ldg(cp + q);
+                        float4 cc = cp[q];
                         v[4 * q + 0] = fmaf(v[4 * q + 0], m, cc.x);
                         v[4 * q + 1] = fmaf(v[4 * q + 1], m, cc.y);
                         v[4 * q + 2] = fmaf(v[4 * q + 2], m, cc.z);
@@ -529,6 +584,10 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         for (int q = 0; q < 32; ++q) dump[row * kp + jc + q] = v[q];
                     }
                     const float lo = fminf(fminf(gmin[0], gmin[1]), fminf(gmin[2], gmin[3]));
+                    if (g_profile_mode == 3) {   // profiling: loads + window arithmetic, no candidate path
+                        if (__float_as_uint(lo) == 0x7fc00001u) flags[0] = 1;
+                        continue;
+                    }
                     if (live && lo <= st.thr) {
                         cand_bound(st, lo);   // the chunk minimum is about to be pushed
 #pragma unroll
@@ -546,8 +605,10 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                 if (lane == 0) {
                     if (CG == 1 || leader) mbar_arrive_local(tempty0 + 8 * acc);
                     else mbar_arrive_cluster(tempty0 + 8 * acc, cl_rank & ~1u);
+                    mbar_arrive_local(cempty0 + 8 * cslot);
                 }
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
+                if (++cslot == CS) { cslot = 0; cphase ^= 1; }
             }
             if (live) {
                 int *out = cand + row * SOMB_CAND_CAP + half * GS;

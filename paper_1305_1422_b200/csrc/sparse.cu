@@ -266,7 +266,8 @@ __global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *
     if (row >= n) return;
     const int64_t e0 = rowptr[row], e1 = rowptr[row + 1];
     int cnt = all ? 0 : ccount[row];
-    const bool scan = all || cnt <= 0;
+    // repaired row (kScanAll), or no candidate anywhere: exact scan of every node
+    const bool scan = all || cnt < 0 || (cnt == 0 && ovf_head[4 * row] < 0);
     if (scan) cnt = K;
     double best = INFINITY;
     int bestj = 0x7fffffff;

@@ -38,7 +38,7 @@ def run(tag, **knobs):
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        _lib.call("somb_bmu_screen", _ptr(eng.Xh), _ptr(eng.Xl), _ptr(eng.xnorm), eng.n, eng.dp, _ptr(eng.Wh),
+        _lib.call("somb_bmu_screen", _ptr(eng.Xh), _ptr(eng.Xl), _ptr(eng.xstat), eng.n, eng.dp, _ptr(eng.Wh),
                   _ptr(eng.Wl), _ptr(eng.c), eng.K, eng.kp, _ptr(eng.scal), C.c_float(eng.window_coef),
                   _ptr(eng.bmu), eng.screen_impl, _ptr(eng.flags), _ptr(eng.ws), _stream(eng.dev))
         b.record()
@@ -54,5 +54,7 @@ if cfgn == "cfg2":
             run(f"multicast {mc} lag {lag}", tc_multicast=mc, screen_lag=lag)
 for lag in (8, 0):
     run(f"{cfgn} passes {eng.passes} lag {lag}", screen_lag=lag)
-run(f"{cfgn} passes {eng.passes} profile (no epilogue)", screen_lag=8, screen_profile=1)
+run(f"{cfgn} passes {eng.passes} profile 1 (no epilogue)", screen_lag=8, screen_profile=1)
+run(f"{cfgn} passes {eng.passes} profile 2 (TMEM loads only)", screen_lag=8, screen_profile=2)
+run(f"{cfgn} passes {eng.passes} profile 3 (loads + window arithmetic)", screen_lag=8, screen_profile=3)
 run("back to normal", screen_lag=8, screen_profile=0)
