@@ -18,8 +18,9 @@
 // (kernels.py:182-192, the final pass of train.py:287-291).
 //
 // Rows whose candidates do not fit (more than GR_C, or a union larger than
-// GR_U) and repaired rows (empty list: exact scan of every node) are
-// re-ranked by their warp straight from global memory, as in rerank_kernel.
+// GR_U) and repaired rows (exact scan of every node) are appended to a
+// device-side row list that the per-row kernels re-rank afterwards (one slow
+// row must not hold 15 warps at the group barrier).
 #include "rerank.cuh"
 
 namespace somb {
@@ -126,68 +127,13 @@ __device__ __forceinline__ void gr_warp_min(double &v, int &j) {
     }
 }
 
-// Global-memory path for one row (warp-collective): its candidate list and
-// spilled entries, or every node when the list is empty.
-template <int MODE>
-__device__ void gr_row_global(int64_t row, const float *__restrict__ X, const double *__restrict__ x2, int d,
-                              const float *__restrict__ W, const double *__restrict__ w2, int K,
-                              const int *__restrict__ cand, const int *__restrict__ ccount, int split,
-                              const OvfView &ov, int lane, int *__restrict__ bmu, double *__restrict__ d2min) {
-    const float *x = X + row * d;
-    const double xx = x2[row];
-    const int cc = ccount[row];
-    const CandLayout L = cand_layout(cc, split, split && ov.ngp ? (int)*ov.ngp : 2);
-    const bool all = cand_scan_all(L, ov, row);
-    double best = INFINITY;
-    int bestj = 0x7fffffff;
-    auto eval = [&](int j) {
-        if ((unsigned)j >= (unsigned)K) return;
-        const float *w = W + (int64_t)j * d;
-        double s = 0.0;
-        if (MODE == SOMB_DIST_NAIVE) {
-            for (int k = lane; k < d; k += 32) {
-                const double df = (double)w[k] - (double)x[k];
-                s = __fma_rn(df, df, s);
-            }
-        } else {
-            for (int k = lane; k < d; k += 32) s = __fma_rn((double)x[k], (double)w[k], s);
-        }
-        s = warp_sum(s);
-        const double v = gr_value<MODE>(s, xx, w2, j);
-        if (v < best || (v == best && j < bestj)) { best = v; bestj = j; }
-    };
-    if (all) {
-        for (int j = 0; j < K; ++j) eval(j);
-    } else {
-        for (int q = 0; q < L.cnt; ++q) eval(cand[row * SOMB_CAND_CAP + cand_slot(L, q)]);
-        if (ov.head != nullptr) {
-            for (int h = 0; h < 4; ++h) {
-                const float lim = ov.lim[4 * row + h];
-                for (int c = ov.head[4 * row + h]; c >= 0; c = ov.next[c]) {
-                    const int m = ov.cnt[c];
-                    const int2 e = lane < m ? ov.ent[(size_t)c * kOvfChunk + lane] : make_int2(0x7f800000, -1);
-                    unsigned bal = __ballot_sync(0xffffffffu, lane < m && __int_as_float(e.x) <= lim);
-                    while (bal) {
-                        const int src = __ffs(bal) - 1;
-                        bal &= bal - 1u;
-                        eval(__shfl_sync(0xffffffffu, e.y, src));
-                    }
-                }
-            }
-        }
-    }
-    if (lane == 0) {
-        bmu[row] = bestj;
-        d2min[row] = best;
-    }
-}
-
 template <int MODE>
 __global__ void __launch_bounds__(GR_THREADS, 1)
 rerank_group_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n, int d,
                     const float *__restrict__ W, const double *__restrict__ w2, int K,
                     const int *__restrict__ cand, const int *__restrict__ ccount, int split,
-                    const int *__restrict__ order, OvfView ov, int *__restrict__ bmu, double *__restrict__ d2min) {
+                    const int *__restrict__ order, OvfView ov, int *__restrict__ bmu, double *__restrict__ d2min,
+                    int *__restrict__ left, unsigned *__restrict__ nleft) {
     extern __shared__ __align__(16) uint8_t gr_raw[];
     GrSmem &S = *reinterpret_cast<GrSmem *>(gr_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -334,8 +280,8 @@ rerank_group_kernel(const float *__restrict__ X, const double *__restrict__ x2, 
                     bmu[row] = bestj;
                     d2min[row] = best;
                 }
-            } else if (T < 0) {
-                gr_row_global<MODE>(row, X, x2, d, W, w2, K, cand, ccount, split, ov, lane, bmu, d2min);
+            } else if (T < 0 && lane == 0) {
+                left[atomicAdd(nleft, 1u)] = (int)row;   // the per-row kernel takes it (bmu.cu)
             }
         }
         __syncthreads();   // the next group rebuilds the shared tables
@@ -346,7 +292,7 @@ size_t rerank_group_smem() { return sizeof(GrSmem); }
 
 int launch_rerank_group(cudaStream_t st, const float *X, const double *x2, int64_t n, int d, const float *W,
                         const double *w2, int K, const int *cand, const int *ccount, int mode, int split,
-                        const int *order, OvfView ov, int *bmu, double *d2min) {
+                        const int *order, OvfView ov, int *bmu, double *d2min, int *left, unsigned *nleft) {
     SOMB_REQUIRE(d % 4 == 0, SOMB_E_INPUT, "rerank_group: d %% 4 required (d=%d)", d);
     static bool init = false;
     const int smem = (int)sizeof(GrSmem);
@@ -366,10 +312,11 @@ int launch_rerank_group(cudaStream_t st, const float *X, const double *x2, int64
     const unsigned blocks = (unsigned)(groups < sms ? groups : sms);
     if (mode == SOMB_DIST_NAIVE)
         rerank_group_kernel<SOMB_DIST_NAIVE><<<blocks, GR_THREADS, smem, st>>>(X, x2, n, d, W, w2, K, cand, ccount,
-                                                                             split, order, ov, bmu, d2min);
+                                                                             split, order, ov, bmu, d2min, left, nleft);
     else
         rerank_group_kernel<SOMB_DIST_BLOCKED><<<blocks, GR_THREADS, smem, st>>>(X, x2, n, d, W, w2, K, cand, ccount,
-                                                                               split, order, ov, bmu, d2min);
+                                                                               split, order, ov, bmu, d2min, left,
+                                                                               nleft);
     note_launch();
     SOMB_LAUNCH_CHECK("rerank_group");
     return SOMB_OK;

@@ -265,6 +265,38 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// two 32-column loads issued back to back, one wait (no load stays in flight
+// past this call)
+__device__ __forceinline__ void tmem_ld32x2(uint32_t ta, float (&va)[32], uint32_t tb, float (&vb)[32]) {
+    uint32_t r[32], q[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(ta));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
+          "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]),
+          "=r"(q[15]), "=r"(q[16]), "=r"(q[17]), "=r"(q[18]), "=r"(q[19]), "=r"(q[20]), "=r"(q[21]),
+          "=r"(q[22]), "=r"(q[23]), "=r"(q[24]), "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]),
+          "=r"(q[29]), "=r"(q[30]), "=r"(q[31])
+        : "r"(tb));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        va[i] = __uint_as_float(r[i]);
+        vb[i] = __uint_as_float(q[i]);
+    }
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -282,6 +314,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 __constant__ int g_profile_mode = 0;
 // 1 = load the data-row (A) tiles with an L2 evict_last policy (SOMB_A_EVICT_LAST, default 0: measured no gain at cfg2)
 __constant__ int g_a_evict_last = 0;
+// 1 = epilogue takes two 32-column chunks per step (SOMB_EPI_PAIR / knob "epi_pair")
+__constant__ int g_epi_pair = 0;
 
 // ------------------------------------------------------------------ kernel
 // MC = 2 (CG = 2 only): clusters of 4 CTAs = 2 pairs on different rows that
@@ -555,20 +589,12 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     continue;
                 }
                 const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN);
-#pragma unroll 1
-                for (int ch = half; ch < TC_BN / 32; ch += Cfg::NGRP) {
-                    float v[32];
-                    tmem_ld32(tbase + ch * 32, v);
-                    if (g_profile_mode == 2) {   // profiling: TMEM loads only
-                        float t = v[0];
-#pragma unroll
-                        for (int q = 1; q < 32; ++q) t = fminf(t, v[q]);
-                        if (__float_as_uint(t) == 0x7fc00001u) flags[0] = 1;   // never: keeps the loads
-                        continue;
-                    }
-                    const int jc = nt * TC_BN + ch * 32;
+                // one 32-column chunk: r = fma(acc, m, c_j), 8-wide group minima,
+                // then the window candidate path
+                // one 32-column chunk: r = fma(acc, m, c_j) and the 8-wide group
+                // minima (arith), then the window candidate path (cands)
+                auto arith = [&](float (&v)[32], int ch, float (&gmin)[4]) {
                     const float4 *cp = reinterpret_cast<const float4 *>(cs + ch * 32);
-                    float gmin[4];   // minima of the four 8-column groups
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         float4 cc = cp[q];
@@ -579,6 +605,9 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         float l4 = fminf(fminf(v[4 * q], v[4 * q + 1]), fminf(v[4 * q + 2], v[4 * q + 3]));
                         gmin[q >> 1] = (q & 1) ? fminf(gmin[q >> 1], l4) : l4;
                     }
+                };
+                auto cands = [&](const float (&v)[32], int ch, const float (&gmin)[4]) {
+                    const int jc = nt * TC_BN + ch * 32;
                     if (dumping) {
 #pragma unroll
                         for (int q = 0; q < 32; ++q) dump[row * kp + jc + q] = v[q];
@@ -586,7 +615,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     const float lo = fminf(fminf(gmin[0], gmin[1]), fminf(gmin[2], gmin[3]));
                     if (g_profile_mode == 3) {   // profiling: loads + window arithmetic, no candidate path
                         if (__float_as_uint(lo) == 0x7fc00001u) flags[0] = 1;
-                        continue;
+                        return;
                     }
                     if (live && lo <= st.thr) {
                         cand_bound(st, lo);   // the chunk minimum is about to be pushed
@@ -599,6 +628,34 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                             }
                         }
                     }
+                };
+                auto tmem_only = [&](const float (&v)[32]) {   // profiling mode 2: TMEM loads only
+                    float t = v[0];
+#pragma unroll
+                    for (int q = 1; q < 32; ++q) t = fminf(t, v[q]);
+                    if (__float_as_uint(t) == 0x7fc00001u) flags[0] = 1;   // never: keeps the loads
+                };
+                if (g_epi_pair) {
+                    // two chunks per step: both TMEM loads issued back to back and
+                    // waited for together, the two chunks' arithmetic interleaved
+#pragma unroll 1
+                    for (int ch = half; ch < TC_BN / 32; ch += 2 * Cfg::NGRP) {
+                        float va[32], vb[32], ga[4], gb[4];
+                        tmem_ld32x2(tbase + ch * 32, va, tbase + (ch + Cfg::NGRP) * 32, vb);
+                        if (g_profile_mode == 2) { tmem_only(va); tmem_only(vb); continue; }
+                        arith(va, ch, ga);
+                        arith(vb, ch + Cfg::NGRP, gb);
+                        cands(va, ch, ga);
+                        cands(vb, ch + Cfg::NGRP, gb);
+                    }
+                } else
+#pragma unroll 1
+                for (int ch = half; ch < TC_BN / 32; ch += Cfg::NGRP) {
+                    float v[32], g[4];
+                    tmem_ld32(tbase + ch * 32, v);
+                    if (g_profile_mode == 2) { tmem_only(v); continue; }
+                    arith(v, ch, g);
+                    cands(v, ch, g);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -720,6 +777,9 @@ static int screen_tc_init() {
     const char *pm = getenv("SOMB_SCREEN_PROFILE");
     int mode = pm ? atoi(pm) : 0;
     cudaMemcpyToSymbol(g_profile_mode, &mode, sizeof(int));
+    const char *ep = getenv("SOMB_EPI_PAIR");
+    int epv = ep ? atoi(ep) : 0;
+    cudaMemcpyToSymbol(g_epi_pair, &epv, sizeof(int));
     const char *ae = getenv("SOMB_A_EVICT_LAST");
     int a_last = ae ? atoi(ae) : 0;
     cudaMemcpyToSymbol(g_a_evict_last, &a_last, sizeof(int));
@@ -748,6 +808,10 @@ int screen_tc_set_knob(const char *key, int value) {
     if (!strcmp(key, "half_cap")) { g_half_cap = value <= 8 ? 8 : value <= 16 ? 16 : 32; return SOMB_OK; }
     if (!strcmp(key, "tc_group")) { g_tc_group = value == 1 ? 1 : 2; return SOMB_OK; }
     if (!strcmp(key, "tc_multicast")) { g_mc = value == 2 ? 2 : 1; return SOMB_OK; }
+    if (!strcmp(key, "epi_pair")) {
+        cudaError_t r = cudaMemcpyToSymbol(g_epi_pair, &value, sizeof(int));
+        return r == cudaSuccess ? SOMB_OK : cuda_status(r, "set epi_pair");
+    }
     if (!strcmp(key, "screen_profile")) {
         cudaError_t r = cudaMemcpyToSymbol(g_profile_mode, &value, sizeof(int));
         return r == cudaSuccess ? SOMB_OK : cuda_status(r, "set screen_profile");
