@@ -265,38 +265,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// two 32-column loads issued back to back, one wait (no load stays in flight
-// past this call)
-__device__ __forceinline__ void tmem_ld32x2(uint32_t ta, float (&va)[32], uint32_t tb, float (&vb)[32]) {
-    uint32_t r[32], q[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(ta));
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
-          "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]),
-          "=r"(q[15]), "=r"(q[16]), "=r"(q[17]), "=r"(q[18]), "=r"(q[19]), "=r"(q[20]), "=r"(q[21]),
-          "=r"(q[22]), "=r"(q[23]), "=r"(q[24]), "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]),
-          "=r"(q[29]), "=r"(q[30]), "=r"(q[31])
-        : "r"(tb));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        va[i] = __uint_as_float(r[i]);
-        vb[i] = __uint_as_float(q[i]);
-    }
-}
-
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -314,8 +282,6 @@ __device__ __forceinline__ void cluster_sync_all() {
 __constant__ int g_profile_mode = 0;
 // 1 = load the data-row (A) tiles with an L2 evict_last policy (SOMB_A_EVICT_LAST, default 0: measured no gain at cfg2)
 __constant__ int g_a_evict_last = 0;
-// 1 = epilogue takes two 32-column chunks per step (SOMB_EPI_PAIR / knob "epi_pair")
-__constant__ int g_epi_pair = 0;
 
 // ------------------------------------------------------------------ kernel
 // MC = 2 (CG = 2 only): clusters of 4 CTAs = 2 pairs on different rows that
@@ -635,20 +601,15 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     for (int q = 1; q < 32; ++q) t = fminf(t, v[q]);
                     if (__float_as_uint(t) == 0x7fc00001u) flags[0] = 1;   // never: keeps the loads
                 };
-                if (g_epi_pair) {
-                    // two chunks per step: both TMEM loads issued back to back and
-                    // waited for together, the two chunks' arithmetic interleaved
-#pragma unroll 1
-                    for (int ch = half; ch < TC_BN / 32; ch += 2 * Cfg::NGRP) {
-                        float va[32], vb[32], ga[4], gb[4];
-                        tmem_ld32x2(tbase + ch * 32, va, tbase + (ch + Cfg::NGRP) * 32, vb);
-                        if (g_profile_mode == 2) { tmem_only(va); tmem_only(vb); continue; }
-                        arith(va, ch, ga);
-                        arith(vb, ch + Cfg::NGRP, gb);
-                        cands(va, ch, ga);
-                        cands(vb, ch + Cfg::NGRP, gb);
-                    }
-                } else
+                // Each chunk's TMEM load is waited for at once: keeping the next
+                // chunk's load in flight while this one is processed (double-
+                // buffered registers) was measured much slower (cfg4 screen
+                // 135 -> 226 ms, cfg5 530 -> 626 ms, tools/ab.sh), and so was
+                // loading two chunks back to back with one wait and interleaving
+                // their arithmetic (cfg4 135 -> 169 ms): longer or overlapping
+                // tcgen05.ld traffic holds up the MMAs on the same SM.  (A 16-warp
+                // epilogue does not launch: 576 threads exceed the 512 the driver
+                // allows this kernel, cudaFuncGetAttributes.)
 #pragma unroll 1
                 for (int ch = half; ch < TC_BN / 32; ch += Cfg::NGRP) {
                     float v[32], g[4];
@@ -777,9 +738,6 @@ static int screen_tc_init() {
     const char *pm = getenv("SOMB_SCREEN_PROFILE");
     int mode = pm ? atoi(pm) : 0;
     cudaMemcpyToSymbol(g_profile_mode, &mode, sizeof(int));
-    const char *ep = getenv("SOMB_EPI_PAIR");
-    int epv = ep ? atoi(ep) : 0;
-    cudaMemcpyToSymbol(g_epi_pair, &epv, sizeof(int));
     const char *ae = getenv("SOMB_A_EVICT_LAST");
     int a_last = ae ? atoi(ae) : 0;
     cudaMemcpyToSymbol(g_a_evict_last, &a_last, sizeof(int));
@@ -808,10 +766,6 @@ int screen_tc_set_knob(const char *key, int value) {
     if (!strcmp(key, "half_cap")) { g_half_cap = value <= 8 ? 8 : value <= 16 ? 16 : 32; return SOMB_OK; }
     if (!strcmp(key, "tc_group")) { g_tc_group = value == 1 ? 1 : 2; return SOMB_OK; }
     if (!strcmp(key, "tc_multicast")) { g_mc = value == 2 ? 2 : 1; return SOMB_OK; }
-    if (!strcmp(key, "epi_pair")) {
-        cudaError_t r = cudaMemcpyToSymbol(g_epi_pair, &value, sizeof(int));
-        return r == cudaSuccess ? SOMB_OK : cuda_status(r, "set epi_pair");
-    }
     if (!strcmp(key, "screen_profile")) {
         cudaError_t r = cudaMemcpyToSymbol(g_profile_mode, &value, sizeof(int));
         return r == cudaSuccess ? SOMB_OK : cuda_status(r, "set screen_profile");
