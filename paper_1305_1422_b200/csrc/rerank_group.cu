@@ -25,33 +25,34 @@
 
 namespace somb {
 
-constexpr int GR_ROWS = 32;                   // rows per group (consecutive in the visiting order)
+constexpr int GR_ROWS = 16;                   // rows per group (consecutive in the visiting order)
 constexpr int GR_WARPS = 16;
 constexpr int GR_THREADS = 32 * GR_WARPS;
 constexpr int GR_RPW = GR_ROWS / GR_WARPS;    // rows per warp
 constexpr int GR_F = 32;                      // features per chunk
 constexpr int GR_FP = GR_F + 4;               // slice pitch in floats (144 B: float4 rows of a quarter-warp hit distinct banks)
-constexpr int GR_U = 512;                     // union capacity (cfg2: union of 32 rows 130-300 mean, p99 <= 442)
+constexpr int GR_NBUF = 4;                    // chunks in flight (cp.async ring): each chunk waits ~one L2 round trip
+constexpr int GR_U = 256;                     // union capacity (cfg2: union of 16 rows 100-210 mean, p99 <= 324)
 constexpr int GR_C = 128;                     // candidates per row evaluated from shared memory
 constexpr int GR_P = GR_C / 32;               // lane passes per row
-constexpr int GR_HASH = 2048;
+constexpr int GR_HASH = 1024;
 
 struct GrSmem {
-    float wb[2][GR_U][GR_FP];                 // union codebook slices (double buffer)
-    float xf[2][GR_ROWS][GR_F];               // data-row slices as loaded
-    double xd[GR_ROWS][GR_F];                 // ... converted to fp64 (odd float4 slices pre-scaled, blocked mode)
+    float wb[GR_NBUF][GR_U][GR_FP];           // union codebook slices (ring)
+    float xf[GR_NBUF][GR_ROWS][GR_F];         // data-row slices as loaded
+    double xd[GR_WARPS][GR_RPW][GR_F];        // ... converted by the row's warp (odd float4 slices pre-scaled, blocked)
     int hkey[GR_HASH];
     int hval[GR_HASH];
     int uid[GR_U];                            // union slot -> node
     unsigned short cs[GR_ROWS][GR_C];         // row's candidates as union slots
-    int rcnt[GR_ROWS];                        // candidates of the row, -1 = global-memory path, 0 = no row
+    int rcnt[GR_ROWS];                        // candidates of the row, -1 = per-row kernel, 0 = no row
     long long rid[GR_ROWS];
     int nu;
 };
 
 // union slot of node j (inserting it); >= GR_U when the union is full
 __device__ __forceinline__ int gr_insert(GrSmem &S, int j) {
-    unsigned h = ((unsigned)j * 2654435761u) >> 21;   // 11 bits
+    unsigned h = ((unsigned)j * 2654435761u) >> 22;   // 10 bits
     for (int probe = 0; probe < GR_HASH; ++probe) {
         const int old = atomicCAS(&S.hkey[h], -1, j);
         if (old == -1) {
@@ -162,50 +163,55 @@ rerank_group_kernel(const float *__restrict__ X, const double *__restrict__ x2, 
         __syncthreads();
         const int nu = S.nu < GR_U ? S.nu : GR_U;
         // ------------------------------------------------ chunked fp64 dots
-        auto issue = [&](int c, int buf) {
-            const int k0 = c * GR_F;
-            const int q4 = (d - k0 < GR_F ? d - k0 : GR_F) >> 2;
-            for (int e = tid; e < nu * q4; e += GR_THREADS) {
-                const int s = e / q4, q = e - s * q4;
-                cp_async16(smem_addr(&S.wb[buf][s][4 * q]), W + (int64_t)S.uid[s] * d + k0 + 4 * q);
+        auto issue = [&](int c) {
+            if (c < nchunks) {
+                const int buf = c % GR_NBUF;
+                const int k0 = c * GR_F;
+                const int q4 = (d - k0 < GR_F ? d - k0 : GR_F) >> 2;
+                for (int e = tid; e < nu * q4; e += GR_THREADS) {
+                    const int s = e / q4, q = e - s * q4;
+                    cp_async16(smem_addr(&S.wb[buf][s][4 * q]), W + (int64_t)S.uid[s] * d + k0 + 4 * q);
+                }
+                for (int e = tid; e < GR_ROWS * q4; e += GR_THREADS) {
+                    const int r = e / q4, q = e - r * q4;
+                    if (S.rcnt[r] > 0) cp_async16(smem_addr(&S.xf[buf][r][4 * q]), X + S.rid[r] * d + k0 + 4 * q);
+                }
             }
-            for (int e = tid; e < GR_ROWS * q4; e += GR_THREADS) {
-                const int r = e / q4, q = e - r * q4;
-                if (S.rcnt[r] > 0) cp_async16(smem_addr(&S.xf[buf][r][4 * q]), X + S.rid[r] * d + k0 + 4 * q);
-            }
-            cp_async_commit();
+            cp_async_commit();   // (empty groups keep the wait_group count uniform)
         };
         double acc[GR_RPW][GR_P][2];
 #pragma unroll
         for (int q = 0; q < GR_RPW; ++q)
 #pragma unroll
             for (int p = 0; p < GR_P; ++p) acc[q][p][0] = acc[q][p][1] = 0.0;
-        issue(0, 0);
+#pragma unroll
+        for (int c = 0; c < GR_NBUF - 1; ++c) issue(c);
 #pragma unroll 1
         for (int c = 0; c < nchunks; ++c) {
-            const int buf = c & 1;
-            cp_async_wait<0>();
-            __syncthreads();   // chunk c landed everywhere; chunk c - 1 fully consumed
-            if (c + 1 < nchunks) issue(c + 1, buf ^ 1);
+            const int buf = c % GR_NBUF;
+            cp_async_wait<GR_NBUF - 2>();
+            __syncthreads();   // chunk c landed everywhere; chunk c - 1 fully consumed (its slot is refilled next)
+            issue(c + GR_NBUF - 1);
             const int kl = d - c * GR_F < GR_F ? d - c * GR_F : GR_F;
-            for (int e = tid; e < GR_ROWS * kl; e += GR_THREADS) {
-                const int r = e / kl, k = e - r * kl;
-                const double sc = (MODE != SOMB_DIST_NAIVE && ((k >> 2) & 1)) ? kF64Scale : 1.0;
-                S.xd[r][k] = (double)S.xf[buf][r][k] * sc;
-            }
-            __syncthreads();
             const int kq = kl >> 2;
 #pragma unroll
             for (int q = 0; q < GR_RPW; ++q) {
                 const int r = warp * GR_RPW + q;
                 const int T = S.rcnt[r];
+                if (T <= 0) continue;   // warp-uniform
+                // the row's slice to fp64, one feature per lane (this warp's own buffer)
+                if (lane < kl) {
+                    const double sc = (MODE != SOMB_DIST_NAIVE && ((lane >> 2) & 1)) ? kF64Scale : 1.0;
+                    S.xd[warp][q][lane] = (double)S.xf[buf][r][lane] * sc;
+                }
+                __syncwarp();
 #pragma unroll
                 for (int p = 0; p < GR_P; ++p) {
                     if (p * 32 >= T) break;   // warp-uniform
                     const int idx = p * 32 + lane;
                     if (idx < T) {
                         const float4 *wp = reinterpret_cast<const float4 *>(S.wb[buf][S.cs[r][idx]]);
-                        const double2 *xp = reinterpret_cast<const double2 *>(S.xd[r]);
+                        const double2 *xp = reinterpret_cast<const double2 *>(S.xd[warp][q]);
                         double a0 = acc[q][p][0], a1 = acc[q][p][1];
                         // even float4 slices: F2F conversions (XU pipe); odd: exact
                         // integer re-exponenting against pre-scaled x (ALU pipe)
@@ -254,8 +260,10 @@ rerank_group_kernel(const float *__restrict__ X, const double *__restrict__ x2, 
                         acc[q][p][1] = a1;
                     }
                 }
+                __syncwarp();   // the next row / chunk overwrites this warp's xd
             }
         }
+        cp_async_wait<0>();
         // ------------------------------------------------------ winners
 #pragma unroll
         for (int q = 0; q < GR_RPW; ++q) {

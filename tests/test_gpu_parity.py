@@ -240,13 +240,20 @@ def test_train_matches_reference_golden(name, screen):
     np.testing.assert_allclose(qes, g[f"{name}_qe"], rtol=1e-6)
 
 
-def test_cfg1_bit_exact_tensor_screen():
-    """Headline parity: cfg1 end to end with the tcgen05 screen reproduces the
-    reference codebook bit for bit (SURVEY.md 7.3-1 recipe)."""
+def test_cfg1_tensor_screen_matches_reference_codebook():
+    """Headline parity: cfg1 end to end with the tcgen05 screen gives the
+    reference's BMU table exactly, and its codebook with at most 0.01% of the
+    entries differing -- each by at most one f32 ulp (the update sums in fp64
+    in a different order than the reference's BLAS, kernels.py:225-226, and
+    the f32 blend rounds the rare last-bit difference either way)."""
     g, x, cb, bmus, u, qes = _run_train_golden("cfg1", "tensor")
-    mism = np.sum(cb.weights != g["cfg1_w"])
-    assert mism <= cb.weights.size * 1e-4, f"{mism} codebook entries differ"
     assert np.array_equal(bmus, g["cfg1_bmus"])
+    ref = np.ascontiguousarray(g["cfg1_w"], dtype=np.float32)
+    got = np.ascontiguousarray(cb.weights, dtype=np.float32)
+    ulps = np.abs(got.view(np.int32).astype(np.int64) - ref.view(np.int32).astype(np.int64))
+    mism = int(np.count_nonzero(ulps))
+    assert mism <= cb.weights.size * 1e-4, f"{mism} codebook entries differ"
+    assert int(ulps.max()) <= 1, f"max difference {int(ulps.max())} ulp"
 
 
 @pytest.mark.parametrize("grid,nbh,compact,mt", [
