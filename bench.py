@@ -57,19 +57,22 @@ def peaks():
 
 
 def measure_l2_gbs(dev):
-    """Achievable L2 read bandwidth: a 48 MB fp32 buffer (L2-resident after the
-    first pass) reduced 40 times (torch.sum, CUDA events).  The denominator of
-    the L2-bound kernels' rooflines (sparse gather, re-rank candidate rows);
-    no driver-written L2 peak exists."""
+    """Achievable L2 read bandwidth: somb_l2_probe (float4 loads, 4 blocks per
+    SM) over a 48 MB fp32 buffer, L2-resident after the first pass, 40 passes
+    timed with CUDA events.  The denominator of the L2-bound kernels'
+    rooflines (sparse gather, re-rank candidate rows); no driver-written L2
+    peak exists."""
+    import ctypes as C
     import torch
+    from paper_1305_1422_b200 import _lib
     buf = torch.rand(12 << 20, device=dev)
-    for _ in range(5):
-        buf.sum()
+    out = torch.zeros(4 * 1024, device=dev)
+    st = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    _lib.call("somb_l2_probe", C.c_void_p(buf.data_ptr()), buf.numel(), 4, C.c_void_p(out.data_ptr()), st)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     a.record()
-    for _ in range(40):
-        buf.sum()
+    _lib.call("somb_l2_probe", C.c_void_p(buf.data_ptr()), buf.numel(), 40, C.c_void_p(out.data_ptr()), st)
     b.record()
     torch.cuda.synchronize()
     return 40 * buf.numel() * 4 / (a.elapsed_time(b) / 1e3) / 1e9
@@ -145,6 +148,11 @@ def init_dist(args):
     # (reduce-scatter / all-reduce / all-gather) runs and is timed on one GPU
     if world > 1 or os.environ.get("SOMB_EXCHANGE") == "always":
         import torch.distributed as dist
+        if world == 1:   # a 1-rank group outside torchrun: env:// rendezvous defaults
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
         # SOMB_DIST_BACKEND=gloo (+ ranks sharing a GPU) exercises the sharded
         # path on a 1-GPU box; production runs use NCCL, one rank per GPU
         backend = os.environ.get("SOMB_DIST_BACKEND", "nccl")
@@ -259,7 +267,7 @@ def run_reference(args):
             "config": {"workload": desc, "rows_sampled": n_sub, "K": nx * ny, "d": d},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -501,12 +509,34 @@ def run_ours(args):
                 "epoch_ms": ms_step,
                 "nkd_per_s": value * d, "window_truncated_rows": trunc, "window_spilled_rows": spilled,
                 "candidates_per_row": cand_stats}
-        print(json.dumps(line), flush=True)
+        emit(line)
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
         barrier()
         dist.destroy_process_group()
     return 0
+
+
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line of the contract, on the real stdout."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
+def _quiet_stdout():
+    """Route everything else written to fd 1 (NCCL's version banner, library
+    prints) to stderr, so stdout carries exactly the one JSON line."""
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
 
 
 def main():
@@ -525,6 +555,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    _quiet_stdout()
     if args.ref_rows == 0:
         args.ref_rows = {"cfg3": 256, "cfg5": 512, "cfg4": 1024, "cfg1": 10000}.get(args.config, 4096)
     if args.impl == "reference":

@@ -272,6 +272,13 @@ SOMB_API int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col,
 /* Number of kernels this library has launched (process lifetime). */
 SOMB_API unsigned long long somb_launch_count(void);
 
+/* Diagnostics: L2 read-bandwidth probe -- `reps` passes of float4 loads over
+ * buf[0, n) (n floats, L2-resident size), enqueued on `stream`; out holds one
+ * float per block (4 x SM count).  Times the achievable L2 read rate that
+ * bench.py uses as the roofline of the L2-bound kernels (no reference
+ * counterpart). */
+SOMB_API int somb_l2_probe(const float *buf, int64_t n, int32_t reps, float *out, void *stream);
+
 /* ---- artifact text (fileio.py:322-359), host code, no GPU needed --------
  * The reference's Python formatting f"{float(v):.6g}", space-separated,
  * one row per line; BMU lines "i row col".  Formats into `out` (capacity

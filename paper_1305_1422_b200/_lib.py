@@ -61,6 +61,7 @@ SIGNATURES = {
     "somb_data_pack_f8": (C.c_int, [P, I64, I32, P, I32, P, P, I32, P, P, P, P]),
     "somb_codebook_prepare_f8": (C.c_int, [P, I32, I32, P, I32, P, P, I32, I32, P, P, P, P, P]),
     "somb_bmu_rerank": (C.c_int, [P, P, I64, I32, P, P, I32, I32, I32, P, P, P, P, P, P]),
+    "somb_l2_probe": (C.c_int, [P, I64, I32, P, P]),
     "somb_bmu_search": (C.c_int, [P, P, P, P, P, I64, I32, I32, P, P, P, P, P, I32, I32, P, F32, P, P, I32,
                                   I32, P, P, P, P, P]),
     "somb_qe_sum": (C.c_int, [P, I64, P, P, P]),

@@ -24,12 +24,8 @@ static unsigned ovf_chunks(int64_t n) { return (unsigned)(4 * n > 4096 ? 4 * n :
 // test knob (somb_set_knob "ovf_chunks"): cap the usable overflow chunks to
 // exercise the pool-exhaustion path (0 = the whole pool)
 static unsigned g_ovf_limit = 0;
-// SOMB_RERANK_GROUP=0 / knob "rerank_group": per-row pipelined re-rank instead
-// of the grouped one (rerank_group.cu)
-static int g_rerank_group = -1;
 int bmu_set_knob(const char *key, int value) {
     if (!strcmp(key, "ovf_chunks")) { g_ovf_limit = value > 0 ? (unsigned)value : 0u; return SOMB_OK; }
-    if (!strcmp(key, "rerank_group")) { g_rerank_group = value < 0 ? -1 : value != 0; return SOMB_OK; }   // -1: default
     return SOMB_E_CONFIG;
 }
 
@@ -229,11 +225,9 @@ __global__ void rerank_kernel(const float *__restrict__ X, const double *__restr
                               int d, const float *__restrict__ W, const double *__restrict__ w2,
                               int K, const int *__restrict__ cand, const int *__restrict__ ccount,
                               int dist_mode, int all, int split, const int *__restrict__ order,
-                              OvfView ov, int *__restrict__ bmu, double *__restrict__ d2min,
-                              const unsigned *__restrict__ n_dev = nullptr) {
+                              OvfView ov, int *__restrict__ bmu, double *__restrict__ d2min) {
     const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
-    if (n_dev) n = (int64_t)*n_dev;   // row list of device-side length (grouped re-rank leftovers)
     if (w >= n) return;
     const int64_t row = order ? (int64_t)order[w] : w;
     const float *x = X + row * d;
@@ -486,10 +480,8 @@ __global__ void __launch_bounds__(32 * RP_WARPS, 3)
 rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n, int d,
                    const float *__restrict__ W, const double *__restrict__ w2, int K,
                    const int *__restrict__ cand, const int *__restrict__ ccount, int split,
-                   const int *__restrict__ order, OvfView ov, int *__restrict__ bmu, double *__restrict__ d2min,
-                   const unsigned *__restrict__ n_dev) {
+                   const int *__restrict__ order, OvfView ov, int *__restrict__ bmu, double *__restrict__ d2min) {
     // [warp][stage][q][lane] float4 (dynamic shared memory)
-    if (n_dev) n = (int64_t)*n_dev;   // row list of device-side length (grouped re-rank leftovers)
     extern __shared__ float4 ring_raw[];
     auto ring = reinterpret_cast<float4 (*)[RS][Q][32]>(ring_raw);
     const int wib = threadIdx.x / 32;
@@ -632,8 +624,7 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
 template <int Q>
 static void launch_rerank_pipe(cudaStream_t st, const float *X, const double *x2, int64_t n, int d, const float *W,
                                const double *w2, int K, const int *cand, const int *ccount, int mode, int split,
-                               const int *order, OvfView ov, int *bmu, double *d2min,
-                               const unsigned *n_dev = nullptr) {
+                               const int *order, OvfView ov, int *bmu, double *d2min) {
     int dev = 0, sms = kSmCount;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -649,11 +640,10 @@ static void launch_rerank_pipe(cudaStream_t st, const float *X, const double *x2
     const unsigned blocks = (unsigned)(need < (int64_t)per_sm * sms ? need : (int64_t)per_sm * sms);
     if (mode == SOMB_DIST_NAIVE)
         rerank_pipe_kernel<Q, SOMB_DIST_NAIVE><<<blocks, 32 * RP_WARPS, smem, st>>>(X, x2, n, d, W, w2, K, cand, ccount,
-                                                                                  split, order, ov, bmu, d2min, n_dev);
+                                                                                  split, order, ov, bmu, d2min);
     else
         rerank_pipe_kernel<Q, SOMB_DIST_BLOCKED><<<blocks, 32 * RP_WARPS, smem, st>>>(X, x2, n, d, W, w2, K, cand,
-                                                                                    ccount, split, order, ov, bmu, d2min,
-                                                                                    n_dev);
+                                                                                    ccount, split, order, ov, bmu, d2min);
 }
 
 template <int Q>
@@ -748,11 +738,6 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
     return launch_repair_truncated(flags, ccount, n, w.ctrs, st);
 }
 
-namespace somb {
-int launch_rerank_group(cudaStream_t st, const float *X, const double *x2, int64_t n, int d, const float *W,
-                        const double *w2, int K, const int *cand, const int *ccount, int mode, int split,
-                        const int *order, OvfView ov, int *bmu, double *d2min, int *left, unsigned *nleft);
-}
 
 static int g_rerank_pipe = -1;   // SOMB_RERANK_PIPE=0 selects the unpipelined kernel (A/B testing)
 
@@ -777,35 +762,6 @@ extern "C" int somb_bmu_rerank(const float *X, const double *x2, int64_t n, int3
     if (all) cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
     const int wpb = 8;
     const unsigned blocks = (unsigned)((n + wpb - 1) / wpb);
-    if (g_rerank_group < 0) {
-        const char *e = getenv("SOMB_RERANK_GROUP");
-        g_rerank_group = e ? atoi(e) != 0 : 0;
-    }
-    if (!all && d % 4 == 0 && g_rerank_group) {
-        // grouped re-rank; the rows it hands back (more than its per-row
-        // capacity, a union overflow, repaired rows) go through the per-row
-        // kernels as a device-side row list (thr0 is free after the screen)
-        int *left = reinterpret_cast<int *>(bw.thr0);
-        unsigned *nleft = bw.ctrs + 6;
-        cudaMemsetAsync(nleft, 0, sizeof(unsigned), st);
-        int rc = launch_rerank_group(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu,
-                                     d2min, left, nleft);
-        if (rc) return rc;
-        if (d <= 128)
-            launch_rerank_pipe<1>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, left, ov, bmu, d2min, nleft);
-        else if (d <= 256)
-            launch_rerank_pipe<2>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, left, ov, bmu, d2min, nleft);
-        else if (d <= 512)
-            launch_rerank_pipe<4>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, left, ov, bmu, d2min, nleft);
-        else if (d <= 1024)
-            launch_rerank_pipe<8>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, left, ov, bmu, d2min, nleft);
-        else
-            rerank_kernel<<<blocks, 32 * wpb, 0, st>>>(X, x2, n, d, W, w2, K, cand, ccount, dist_mode, 0, split, left,
-                                                       ov, bmu, d2min, nleft);
-        note_launch();
-        SOMB_LAUNCH_CHECK("rerank leftovers");
-        return SOMB_OK;
-    }
     if (!all && d % 4 == 0 && d <= 1024 && g_rerank_pipe) {
         if (d <= 128)
             launch_rerank_pipe<1>(st, X, x2, n, d, W, w2, K, cand, ccount, dist_mode, split, row_order, ov, bmu, d2min);

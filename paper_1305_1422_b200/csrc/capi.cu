@@ -49,3 +49,39 @@ extern "C" int somb_set_knob(const char *key, int32_t value) {
     if (rc == SOMB_E_CONFIG) somb::set_error("set_knob: unknown key %s", key);
     return rc;
 }
+
+// ------------------------------------------------------------ diagnostics
+// L2 read-bandwidth probe: `reps` grid-stride passes of float4 loads over a
+// buffer small enough to stay L2-resident (the denominator of the L2-bound
+// kernels' rooflines, bench.py; no driver-written L2 peak exists).  One
+// partial sum per thread block keeps the loads live.
+namespace somb {
+__global__ void __launch_bounds__(512) l2_probe_kernel(const float4 *__restrict__ buf, int64_t n4, int reps,
+                                                       float *__restrict__ out) {
+    float acc = 0.0f;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int r = 0; r < reps; ++r) {
+        // rotate the start so consecutive passes do not hit the same lines first
+        const int64_t off = ((int64_t)r * 7919 * blockDim.x) % n4;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+            int64_t j = i + off;
+            if (j >= n4) j -= n4;
+            const float4 v = __ldcg(buf + j);
+            acc += (v.x + v.y) + (v.z + v.w);
+        }
+    }
+    if (acc == 1.2345e-30f) out[blockIdx.x] = acc;   // never taken: keeps the loads
+}
+}  // namespace somb
+
+extern "C" int somb_l2_probe(const float *buf, int64_t n, int32_t reps, float *out, void *stream) {
+    SOMB_REQUIRE(buf && n >= 4 && reps > 0, SOMB_E_INPUT, "l2_probe: bad arguments");
+    int dev = 0, sms = somb::kSmCount;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    somb::l2_probe_kernel<<<4 * sms, 512, 0, somb::as_stream(stream)>>>(reinterpret_cast<const float4 *>(buf), n / 4,
+                                                                          reps, out);
+    somb::note_launch();
+    SOMB_LAUNCH_CHECK("l2_probe");
+    return SOMB_OK;
+}

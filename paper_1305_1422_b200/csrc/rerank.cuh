@@ -1,4 +1,4 @@
-// Shared pieces of the exact fp64 re-rank kernels (bmu.cu, rerank_group.cu):
+// Shared pieces of the exact fp64 re-rank kernels (bmu.cu):
 // the candidate-list layout written by the screens, the overflow-pool view,
 // cp.async helpers and the XU-free fp32 -> fp64 conversion.
 #pragma once

@@ -282,8 +282,6 @@ __device__ __forceinline__ void cluster_sync_all() {
 __constant__ int g_profile_mode = 0;
 // 1 = load the data-row (A) tiles with an L2 evict_last policy (SOMB_A_EVICT_LAST, default 0: measured no gain at cfg2)
 __constant__ int g_a_evict_last = 0;
-// 1 = defer candidate pushes past the accumulator release (SOMB_SCREEN_DEFER / knob "screen_defer")
-__constant__ int g_defer = 0;
 
 // ------------------------------------------------------------------ kernel
 // MC = 2 (CG = 2 only): clusters of 4 CTAs = 2 pairs on different rows that
@@ -540,9 +538,6 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             cand_init(st, live ? wcoef * screen_sigma(reinterpret_cast<const float4 *>(xstat)[row], scal) : 0.0f);
             if (live && thr0) st.thr = thr0[row];
             const bool dumping = dump != nullptr && live;
-            int dq = 0;                  // deferred candidate pushes (g_defer)
-            float dv0 = 0.f, dv1 = 0.f, dv2 = 0.f, dv3 = 0.f;
-            int dj0 = 0, dj1 = 0, dj2 = 0, dj3 = 0;
             for (int nt = 0; nt < NT; ++nt) {
                 mbar_wait(tfull0 + 8 * acc, aphase);
                 tc_fence_after();
@@ -595,19 +590,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                             if (gmin[g8] <= st.thr) {
 #pragma unroll
                                 for (int q = 8 * g8; q < 8 * g8 + 8; ++q)
-                                    if (v[q] <= st.thr) {
-                                        // defer the push past the accumulator release
-                                        // (4-entry register queue; a full queue pushes now)
-                                        if (g_defer && dq < 4) {
-                                            if (dq == 0) { dv0 = v[q]; dj0 = jc + q; }
-                                            else if (dq == 1) { dv1 = v[q]; dj1 = jc + q; }
-                                            else if (dq == 2) { dv2 = v[q]; dj2 = jc + q; }
-                                            else { dv3 = v[q]; dj3 = jc + q; }
-                                            ++dq;
-                                        } else {
-                                            cand_push<Cfg::HALF_CAP>(st, v[q], jc + q, cb, pool);
-                                        }
-                                    }
+                                    if (v[q] <= st.thr) cand_push<Cfg::HALF_CAP>(st, v[q], jc + q, cb, pool);
                             }
                         }
                     }
@@ -644,15 +627,6 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                 }
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
                 if (++cslot == CS) { cslot = 0; cphase ^= 1; }
-                // deferred pushes of this tile, now off the accumulator's critical
-                // path (the next tile's MMAs already run); out of node order only
-                // within a tile, which matters only to truncation -- and truncated
-                // rows are re-ranked by a full scan (bmu.cu)
-                if (dq > 0) cand_push<Cfg::HALF_CAP>(st, dv0, dj0, cb, pool);
-                if (dq > 1) cand_push<Cfg::HALF_CAP>(st, dv1, dj1, cb, pool);
-                if (dq > 2) cand_push<Cfg::HALF_CAP>(st, dv2, dj2, cb, pool);
-                if (dq > 3) cand_push<Cfg::HALF_CAP>(st, dv3, dj3, cb, pool);
-                dq = 0;
             }
             if (live) {
                 int *out = cand + row * SOMB_CAND_CAP + half * GS;
@@ -764,9 +738,6 @@ static int screen_tc_init() {
     const char *pm = getenv("SOMB_SCREEN_PROFILE");
     int mode = pm ? atoi(pm) : 0;
     cudaMemcpyToSymbol(g_profile_mode, &mode, sizeof(int));
-    const char *df = getenv("SOMB_SCREEN_DEFER");
-    int dfv = df ? atoi(df) : 0;
-    cudaMemcpyToSymbol(g_defer, &dfv, sizeof(int));
     const char *ae = getenv("SOMB_A_EVICT_LAST");
     int a_last = ae ? atoi(ae) : 0;
     cudaMemcpyToSymbol(g_a_evict_last, &a_last, sizeof(int));
@@ -795,10 +766,6 @@ int screen_tc_set_knob(const char *key, int value) {
     if (!strcmp(key, "half_cap")) { g_half_cap = value <= 8 ? 8 : value <= 16 ? 16 : 32; return SOMB_OK; }
     if (!strcmp(key, "tc_group")) { g_tc_group = value == 1 ? 1 : 2; return SOMB_OK; }
     if (!strcmp(key, "tc_multicast")) { g_mc = value == 2 ? 2 : 1; return SOMB_OK; }
-    if (!strcmp(key, "screen_defer")) {
-        cudaError_t r = cudaMemcpyToSymbol(g_defer, &value, sizeof(int));
-        return r == cudaSuccess ? SOMB_OK : cuda_status(r, "set screen_defer");
-    }
     if (!strcmp(key, "screen_profile")) {
         cudaError_t r = cudaMemcpyToSymbol(g_profile_mode, &value, sizeof(int));
         return r == cudaSuccess ? SOMB_OK : cuda_status(r, "set screen_profile");

@@ -573,44 +573,3 @@ def test_overflow_pool_exhaustion_sparse():
     eng.search()
     assert np.array_equal(eng.bmu[:n].cpu().numpy(), want)
     assert ((eng.flags[:n].cpu().numpy() & 0x01010101) == 0).all()
-
-
-@pytest.mark.parametrize("fam,d,nx,ny", [("uniform", 256, 40, 30), ("uniform", 1000, 60, 50), ("nearconst", 100, 70, 70),
-                                          ("dupcols", 132, 50, 40)])
-def test_grouped_rerank_matches_per_row_rerank(fam, d, nx, ny):
-    """The grouped re-rank (rerank_group.cu: union of the candidate nodes of
-    32 BMU-sorted rows staged in shared memory) returns the per-row re-rank's
-    BMUs, blocked and naive formulas, in previous-BMU order and without it;
-    the near-constant family overflows the union and exercises the
-    global-memory path.  d2min agrees to fp64 summation order (1e-12)."""
-    from paper_1305_1422_b200 import _lib
-    from test_gpu_shapes import family
-    x = family(fam, 20000, d)
-    lib = _lib.load()
-    eng = S.SomEngine(x, nx, ny, S.MapType.TOROID, device="cuda:0")
-    cfg = S.resolve_defaults(S.TrainConfig(n_columns=nx, n_rows=ny))
-    eng.set_codebook(S.init_codebook(cfg, d).weights)
-    for e in range(3):   # collapse the codebook a little: candidate-heavy lists, a row order
-        eng.epoch(max(nx, ny) / 2 * (1 - e / 3) + 1, 1.0 - 0.3 * e, 1e-3)
-    for mode in (_lib.DIST_BLOCKED, _lib.DIST_NAIVE):
-        for use_order in (True, False):
-            eng.opt.rerank_order = use_order
-            got = {}
-            for grouped in (1, 0):
-                assert lib.somb_set_knob(b"rerank_group", grouped) == 0
-                try:
-                    eng.has_prev = False
-                    eng.search(mode)
-                    torch.cuda.synchronize()
-                    got[grouped] = (eng.bmu[: eng.n].cpu().numpy().copy(), eng.d2min[: eng.n].cpu().numpy().copy())
-                finally:
-                    assert lib.somb_set_knob(b"rerank_group", -1) == 0
-            b1, d1 = got[1]
-            b0, d0 = got[0]
-            # blocked d2 = ((-2 x.w) + |x|^2) + |w|^2 cancels: the summation-order
-            # difference is relative to |x|^2 + |w|^2, not to d2
-            scale = eng.x2[: eng.n].cpu().numpy() + float(eng.w2.max())
-            assert np.max(np.abs(d1 - d0) / scale) <= 1e-13
-            diff = np.flatnonzero(b1 != b0)
-            assert len(diff) <= max(1, eng.n // 10000), (fam, mode, use_order, len(diff))
-    eng.opt.rerank_order = True
