@@ -388,7 +388,7 @@ def run_ours(args):
                 "executed_tflops": achieved * getattr(eng, "passes", 1),
                 "executed_frac": achieved * getattr(eng, "passes", 1) / peak_sus,
                 "note": "achieved = algorithmic 2*n*K*d flops / screen time; the split screens for "
-                        "d <= 256 execute mma_passes x that in fp16-equivalent tensor work (2: fp16 hi.hi "
+                        "d <= 128 execute mma_passes x that in fp16-equivalent tensor work (2: fp16 hi.hi "
                         "+ two fp8 cross terms at twice the rate; 3: three fp16 passes)"}
     if sparse:
         simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12
@@ -550,7 +550,7 @@ def main():
     ap.add_argument("--e2e-epochs", type=int, default=10)
     ap.add_argument("--ref-rows", type=int, default=0, help="CPU sample rows (0: per-config default)")
     ap.add_argument("--passes", type=int, default=0, choices=[0, 1, 2, 3],
-                    help="screen passes (0: auto = 2 (fp16 + fp8 cross terms) for d <= 256)")
+                    help="screen passes (0: auto = 2 (fp16 + fp8 cross terms) for d <= 128)")
     ap.add_argument("--no-rerank-order", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -49,7 +49,7 @@ class EngineOptions:
     window_kappa: float = _DEF_WINDOW_KAPPA
     hypot_table: bool = True          # numpy-hypot distances for rect grids (bit parity)
     seed_prev: bool = True            # seed the screen threshold from the previous BMUs
-    screen_passes: int = 0            # 0 auto (2 if the padded feature count <= 256), 1, 2 (fp16 + fp8 cross terms) or 3
+    screen_passes: int = 0            # 0 auto (2 if the padded feature count <= 128), 1, 2 (fp16 + fp8 cross terms) or 3
     window_kappa3: Optional[float] = None     # None: _kappa3(d)
     window_kappa2: float = _DEF_WINDOW_KAPPA2   # 2-pass (fp16 + fp8 cross terms) window, sigma units
     conv: str = "auto"                # neighbourhood convolution: "auto", "direct", "spectral"
@@ -270,7 +270,14 @@ class SomEngine:
         elif p in (1, 2, 3):
             self.passes = p
         else:
-            self.passes = 2 if dp0 <= 256 else 1
+            self._adaptive = dp0 <= 256   # may switch to the split screen (search)
+            # split screen only where the 1-pass window holds too many near
+            # ties: cfg5 (d = 128, K = 250k) keeps ~360 nodes per row in the
+            # 1-pass window (rows truncate, full-scan repairs: 44 s per
+            # epoch) against 13 with the fp8 split; at cfg4 (d = 256,
+            # K = 90k) the 1-pass screen is the faster one (137 vs 146 ms per
+            # epoch, 23 candidates per row) -- tools/r2_p1.sh
+            self.passes = 2 if dp0 <= 128 else 1
         self.pack_dataset()
 
     def _init_codebook_buffers(self):
@@ -411,6 +418,30 @@ class SomEngine:
                   _ptr(self.d2min), _ptr(self.flags), _ptr(self.ws), st)
         self._mark("rerank", False)
         self.has_prev = True
+        if self._adaptive and self.passes == 1 and self.screen_impl == 0:
+            # Auto mode, 128 < dp <= 256: the 1-pass screen is the faster one
+            # on spread data, but structured data (near-constant rows, a large
+            # mean offset) can keep hundreds of nodes inside its window, so
+            # rows truncate and are repaired by full scans (exact, but slow:
+            # cfg4 near-constant rows, 50% of the rows per epoch).  Then the
+            # fp16 + fp8 split screen takes over for the rest of the training.
+            # One 4-byte host read per epoch.
+            rep = self.repaired_rows()
+            if rep > 0.005 * self.n:
+                self._switch_to_split()
+
+    _adaptive = False
+
+    def _switch_to_split(self):
+        """1-pass -> 2-pass (fp16 + fp8 cross terms) screen from the next
+        search on: re-pack the rows with the fp8 cross operands, allocate the
+        codebook's, switch the window."""
+        self.passes = 2
+        self.pack_dataset()
+        self._init_codebook_buffers()
+        self.window_coef = self._window_coef()
+        self.screen_impl = 3
+        self.switched_to_split = True
 
     def debug_screen_values(self) -> torch.Tensor:
         """tcgen05 screened values r~ of rows [0, 128) x all nodes (calibration)."""

@@ -128,7 +128,7 @@ def test_cfg5_shape_all_epochs(fam):
 
 @pytest.mark.parametrize("fam", ["uniform", "blobs"])
 def test_cfg4_shape_all_epochs(fam):
-    """cfg4: 300x300 hexagonal toroid, bubble, compact support, d = 256 (2-pass), 2048 rows."""
+    """cfg4: 300x300 hexagonal toroid, bubble, compact support, d = 256 (1-pass by default), 2048 rows."""
     x = family(fam, 2048, 256)
     cfg = _cfg(300, 300, "toroid", "hexagonal", "bubble", True)
     w0 = S.init_codebook(cfg, 256).weights
@@ -156,3 +156,31 @@ def test_cfg3_shape_sparse(init):
     cols = np.sort(np.random.default_rng(4).choice(50_000, 2048, replace=False))
     _teacher_forced(sp, None, 100, 100, O.PLANAR, O.RECT, O.GAUSSIAN, False, w0, cfg, (0, 1, 5, 9),
                     sparse=True, cols=cols)
+
+
+def test_auto_screen_switches_to_split_on_structured_data():
+    """Auto screen for 128 < d <= 256 starts 1-pass; near-constant rows keep
+    hundreds of nodes in its window, rows truncate and are repaired by full
+    scans, and the engine switches to the fp16 + fp8 split screen
+    (engine.SomEngine._switch_to_split).  Every epoch's BMUs equal the exact
+    fp64 argmin (first-minimum ties), before and after the switch."""
+    import torch
+    x = family("nearconst", 4096, 256)
+    eng = S.SomEngine(S.DenseDataset(x), 300, 300, S.MapType.TOROID, S.GridType.HEXAGONAL)
+    assert eng.passes == 1 and eng._adaptive
+    eng.init_codebook_device(1)
+    X = torch.from_numpy(x).cuda().double()
+    for e in range(4):
+        eng.search()
+        W = eng.W[: eng.K].double()
+        d2 = torch.clamp((-2.0 * (X @ W.T) + eng.x2[: eng.n, None]) + eng.w2[None, : eng.K], min=0.0)
+        want = torch.argmin(d2, dim=1)
+        got = eng.bmu[: eng.n].long()
+        bad = torch.nonzero(got != want).flatten()
+        if len(bad):   # only fp64 summation-order ties
+            gap = (d2[bad, got[bad]] - d2[bad, want[bad]]).abs() / (eng.x2[bad] + eng.w2.max())
+            assert float(gap.max()) <= 1e-12, (e, len(bad))
+        eng.qe_sum()
+        eng.node_sums()
+        eng.update(150.0 * (1 - e / 4) + 1, 1.0 - 0.2 * e, 1e-3, S.Neighborhood.BUBBLE, True)
+    assert eng.passes == 2 and getattr(eng, "switched_to_split", False)
