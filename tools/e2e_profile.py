@@ -1,5 +1,5 @@
 """Where does the end-to-end train() time go?  Replays train()'s steps for the
-cfg2 workload from pinned host rows with a sync + wall clock after each.
+cfg2 workload from pageable numpy rows with a sync + wall clock after each.
    python tools/e2e_profile.py"""
 import os
 import sys
@@ -15,10 +15,7 @@ from paper_1305_1422_b200.kernels import make_engine  # noqa: E402
 from paper_1305_1422_b200.train import _to_coords  # noqa: E402
 
 n, d, nx, ny = 1_000_000, 1000, 200, 200
-g = torch.Generator(device="cuda")
-g.manual_seed(1001)
-Xh = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
-Xh.copy_(torch.rand((n, d), generator=g, device="cuda"))
+Xh = np.random.default_rng(1001).random((n, d), dtype=np.float32)   # pageable numpy, as a reference user passes it
 cfg = S.resolve_defaults(S.TrainConfig(n_epochs=10, n_columns=nx, n_rows=ny, map_type=S.MapType.TOROID))
 for rep in range(2):
     torch.cuda.synchronize()
