@@ -51,7 +51,11 @@ constexpr int TC_ROWS = 128;                      // data rows per CTA (TMEM lan
 // D += hi.hi + hi.lo + lo.hi (~22-bit operand precision, 3x the MMAs) for
 // small feature counts where the 1-pass fp16 window holds too many
 // near-tied nodes.  A stage holds [A_hi | B_hi | A_lo | B_lo].
-template <int CG, int PASSES = 1, int HC = SOMB_CAND_CAP / 2, int EPI = TC_EPI_WARPS>
+// AR = 1: the CTA's data-row (A) operands stay resident in shared memory for
+// a whole unit (all node tiles of its 128 rows); only codebook (B) tiles
+// stream through the stage ring.  For K-chunk counts <= 4 (d <= 256 1-pass,
+// d <= 128 2-pass), where A would otherwise be re-read from L2 per tile.
+template <int CG, int PASSES = 1, int HC = SOMB_CAND_CAP / 2, int EPI = TC_EPI_WARPS, int AR = 0>
 struct TcCfg {
     static constexpr int EPI_WARPS = EPI;                           // 8 (2 column groups) or 16 (4 groups)
     static constexpr int NGRP = EPI / 4;                            // column groups per row
@@ -59,7 +63,10 @@ struct TcCfg {
     static constexpr int B_ROWS = TC_BN / CG;                      // codebook rows per CTA (smem B tile)
     static constexpr uint32_t A_BYTES = TC_ROWS * TC_BK * 2;       // 16 KB
     static constexpr uint32_t B_BYTES = B_ROWS * TC_BK * 2;        // 32 KB (CG 1) / 16 KB (CG 2)
-    static constexpr uint32_t STAGE_BYTES = (PASSES == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
+    static_assert(!AR || PASSES != 3, "A-resident mode: 1- or 2-pass");
+    static constexpr uint32_t STAGE_BYTES = AR ? B_BYTES : (PASSES == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
+    static constexpr int A_CHUNKS = 4;                                 // resident A: <= 4 K-chunks
+    static constexpr uint32_t ARES_BYTES = AR ? A_CHUNKS * A_BYTES : 0;
     // candidates kept per (row, column group): HC (<= SOMB_CAND_CAP / 2) in
     // shared memory; when a group's window holds more, its 3 HC / 4 lowest
     // screened (value, index) pairs are kept (cand.cuh)
@@ -76,10 +83,10 @@ struct TcCfg {
     // the dynamic shared window is 1024-byte aligned (declared __align__(1024),
     // checked at kernel start), so the whole opt-in maximum is usable
     static constexpr uint32_t SMEM_MAX = 232448;
-    static constexpr int STAGES_RAW = (int)((SMEM_MAX - CAND_BYTES - C_BYTES - BAR_BYTES) / STAGE_BYTES);
+    static constexpr int STAGES_RAW = (int)((SMEM_MAX - ARES_BYTES - CAND_BYTES - C_BYTES - BAR_BYTES) / STAGE_BYTES);
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static_assert(STAGES >= 2, "pipeline needs two stages");
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + CAND_BYTES + C_BYTES + BAR_BYTES;
+    static constexpr uint32_t SMEM = ARES_BYTES + STAGES * STAGE_BYTES + CAND_BYTES + C_BYTES + BAR_BYTES;
     // kind::f16 instruction descriptor: A,B = f16, D = f32, K-major, M = 128 CG, N = 256
     static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((128 * CG) >> 4) << 24);
 };
@@ -290,7 +297,7 @@ __constant__ int g_a_evict_last = 0;
 // the L2 -> SM codebook traffic halves (the screen is L2-bandwidth bound).
 // Both pairs' MMAs must release a stage before it is refilled (empty
 // barriers count MC arrivals).
-template <int CG, int PASSES, int HC, int MC = 1, int EPI = TC_EPI_WARPS>
+template <int CG, int PASSES, int HC, int MC = 1, int EPI = TC_EPI_WARPS, int AR = 0>
 __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const CUtensorMap *map_w,
                                                const CUtensorMap *map_xl, const CUtensorMap *map_wl, int64_t n,
                                                int dp, int kp, const float *__restrict__ c,
@@ -300,20 +307,23 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                                                float *__restrict__ dump, unsigned *__restrict__ sync_ctr,
                                                int lag, OvfPool pool, int *__restrict__ ovf_head,
                                                float *__restrict__ ovf_lim) {
-    using Cfg = TcCfg<CG, PASSES, HC, EPI>;
+    using Cfg = TcCfg<CG, PASSES, HC, EPI, AR>;
+    static_assert(!AR || MC == 1, "A-resident mode without codebook multicast");
     constexpr int S = Cfg::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = smem_raw;
     if (smem_u32(smem_raw) & 1023u) __trap();   // SWIZZLE_128B tiles need 1024-byte alignment
+    uint8_t *ares = smem_raw;                    // resident A chunks (AR)
+    uint8_t *smem = smem_raw + Cfg::ARES_BYTES;  // stage ring
     // stage s: A_hi at smem + s*STAGE_BYTES, B_hi after it, then A_lo, B_lo (3-pass)
     float *cbv = (float *)(smem + S * Cfg::STAGE_BYTES);
     int *cbi = (int *)(cbv + EPI * 32 * Cfg::HALF_CAP);
     float *cring = (float *)(smem + S * Cfg::STAGE_BYTES + Cfg::CAND_BYTES);
     uint64_t *bars = (uint64_t *)(smem + S * Cfg::STAGE_BYTES + Cfg::CAND_BYTES + Cfg::C_BYTES);
-    // bars: full[S] empty[S] tfull[2] tempty[2] cfull[C_SLOTS] cempty[C_SLOTS]; then the TMEM base address
+    // bars: full[S] empty[S] tfull[2] tempty[2] cfull[C_SLOTS] cempty[C_SLOTS] afull aempty;
+    // then the TMEM base address
     constexpr int CS = Cfg::C_SLOTS;
-    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * S + 4 + 2 * CS);
-    static_assert((2 * S + 4 + 2 * CS) * 8 + 4 <= (int)Cfg::BAR_BYTES, "barrier area");
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * S + 4 + 2 * CS + 2);
+    static_assert((2 * S + 4 + 2 * CS + 2) * 8 + 4 <= (int)Cfg::BAR_BYTES, "barrier area");
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
     const uint32_t cl_rank = CG == 2 ? cluster_rank() : 0;
@@ -324,6 +334,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t tfull0 = smem_u32(bars + 2 * S), tempty0 = smem_u32(bars + 2 * S + 2);
     const uint32_t cfull0 = smem_u32(bars + 2 * S + 4), cempty0 = smem_u32(bars + 2 * S + 4 + CS);
+    const uint32_t afull = smem_u32(bars + 2 * S + 4 + 2 * CS), aempty = afull + 8;
 
     if (threadIdx.x == 0 && blockIdx.x == 0) sync_ctr[3] = Cfg::NGRP;   // candidate-list layout for the re-rank
     if (threadIdx.x == 0) {
@@ -339,6 +350,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             mbar_init(cfull0 + 8 * a, 1);           // the producer's expect_tx
             mbar_init(cempty0 + 8 * a, EPI);        // one arrival per epilogue warp of this CTA
         }
+        mbar_init(afull, 1);                        // resident A loaded (leader's expect_tx)
+        mbar_init(aempty, 1);                       // the unit's last MMAs retired (leader's commit)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map_x)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map_w)) : "memory");
@@ -384,9 +397,19 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             const unsigned P = gridDim.x;
             const int waves = (num_units + unit_step - 1) / unit_step;
             unsigned issued = 0;
+            uint32_t arph = 0;
             for (int it = 0; it < (MC == 1 ? (unit0 < num_units ? (num_units - unit0 + unit_step - 1) / unit_step : 0) : iters); ++it) {
                 const int u = unit0 + it * unit_step;
                 const int row0 = u * unit_rows + TC_ROWS * (int)crank;
+                if constexpr (AR) {   // this unit's A chunks, once (after the previous unit's MMAs retired)
+                    mbar_wait(aempty, arph ^ 1);
+                    if (leader) mbar_expect_tx(afull, CG * (KB8 + KB) * Cfg::A_BYTES);
+                    for (int kb = 0; kb < KB8; ++kb)
+                        tma_load_2d<CG>(smem_u32(ares + kb * Cfg::A_BYTES), map_xl, afull, kb * 128, row0);
+                    for (int kb = 0; kb < KB; ++kb)
+                        tma_load_2d<CG>(smem_u32(ares + (KB8 + kb) * Cfg::A_BYTES), map_x, afull, kb * TC_BK, row0);
+                    arph ^= 1;
+                }
                 for (int nt = 0; nt < NT; ++nt) {
                     if (lag > 0 && issued > (unsigned)lag) {
                         const unsigned need = P * (issued - (unsigned)lag);
@@ -411,14 +434,17 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         const uint32_t fb = full0 + 8 * stage;
                         if (leader) mbar_expect_tx(fb, CG * Cfg::STAGE_BYTES);
                         uint8_t *st0 = smem + stage * Cfg::STAGE_BYTES;
-                        tma_load_2d<CG>(smem_u32(st0), map_xl, fb, kb * 128, row0);
-                        if constexpr (MC == 1) {
+                        if constexpr (AR) {
+                            tma_load_2d<CG>(smem_u32(st0), map_wl, fb, kb * 128, node0);
+                        } else if constexpr (MC == 1) {
+                            tma_load_2d<CG>(smem_u32(st0), map_xl, fb, kb * 128, row0);
                             tma_load_2d<CG>(smem_u32(st0 + Cfg::A_BYTES), map_wl, fb, kb * 128, node0);
                         } else {
-                            const uint32_t sub = (uint32_t)pair * (Cfg::B_BYTES / MC);
+                            tma_load_2d<CG>(smem_u32(st0), map_xl, fb, kb * 128, row0);
+                            const uint32_t sub = (uint32_t)pair * (Cfg::B_BYTES / 2);
                             const uint16_t mcm = (uint16_t)((1u << crank) | (1u << (crank + 2)));
                             tma_load_2d_mc(smem_u32(st0 + Cfg::A_BYTES + sub), map_wl, fb, kb * 128,
-                                           node0 + (Cfg::B_ROWS / MC) * (int)pair, mcm);
+                                           node0 + (Cfg::B_ROWS / 2) * (int)pair, mcm);
                         }
                         if (++stage == S) { stage = 0; phase ^= 1; }
                     }
@@ -427,11 +453,15 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                         const uint32_t fb = full0 + 8 * stage;
                         if (leader) mbar_expect_tx(fb, CG * Cfg::STAGE_BYTES);
                         uint8_t *st0 = smem + stage * Cfg::STAGE_BYTES;
-                        if (hint_a)
-                            tma_load_2d_hint<CG>(smem_u32(st0), map_x, fb, kb * TC_BK, row0, pol_a);
-                        else
-                            tma_load_2d<CG>(smem_u32(st0), map_x, fb, kb * TC_BK, row0);
-                        if constexpr (MC == 1) {
+                        if constexpr (!AR) {
+                            if (hint_a)
+                                tma_load_2d_hint<CG>(smem_u32(st0), map_x, fb, kb * TC_BK, row0, pol_a);
+                            else
+                                tma_load_2d<CG>(smem_u32(st0), map_x, fb, kb * TC_BK, row0);
+                        }
+                        if constexpr (AR) {
+                            tma_load_2d<CG>(smem_u32(st0), map_w, fb, kb * TC_BK, node0);
+                        } else if constexpr (MC == 1) {
                             tma_load_2d<CG>(smem_u32(st0 + Cfg::A_BYTES), map_w, fb, kb * TC_BK, node0);
                         } else {   // my sub-box of the pair-half, multicast to the same rank of both pairs
                             const uint32_t sub = (uint32_t)pair * (Cfg::B_BYTES / MC);
@@ -471,7 +501,13 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
             int acc = 0;
             uint32_t aphase = 0;
             const int my_iters = MC == 1 ? (unit0 < num_units ? (num_units - unit0 + unit_step - 1) / unit_step : 0) : iters;
+            uint32_t arph = 0;
             for (int it = 0; it < my_iters; ++it) {
+                if constexpr (AR) {   // this unit's resident A chunks have landed (both CTAs)
+                    mbar_wait(afull, arph);
+                    tc_fence_after();
+                    arph ^= 1;
+                }
                 for (int nt = 0; nt < NT; ++nt) {
                     mbar_wait(tempty0 + 8 * acc, aphase ^ 1);
                     tc_fence_after();
@@ -479,8 +515,8 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     for (int kb = 0; kb < KB8; ++kb) {   // fp8 cross terms, accumulated from zero
                         mbar_wait(full0 + 8 * stage, phase);
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-                        const uint32_t b0 = a0 + Cfg::A_BYTES;
+                        const uint32_t a0 = AR ? smem_u32(ares + kb * Cfg::A_BYTES) : smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                        const uint32_t b0 = AR ? smem_u32(smem + stage * Cfg::STAGE_BYTES) : a0 + Cfg::A_BYTES;
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             tc_mma_f8<CG>(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), Cfg::IDESC,
@@ -491,8 +527,9 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     for (int kb = 0; kb < KB; ++kb) {
                         mbar_wait(full0 + 8 * stage, phase);
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-                        const uint32_t b0 = a0 + Cfg::A_BYTES;
+                        const uint32_t a0 = AR ? smem_u32(ares + (KB8 + kb) * Cfg::A_BYTES)
+                                               : smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                        const uint32_t b0 = AR ? smem_u32(smem + stage * Cfg::STAGE_BYTES) : a0 + Cfg::A_BYTES;
 #pragma unroll
                         for (int k = 0; k < TC_BK / TC_UMMA_K; ++k) {
                             tc_mma_f16<CG>(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), Cfg::IDESC,
@@ -509,6 +546,7 @@ __device__ __forceinline__ void screen_tc_body(const CUtensorMap *map_x, const C
                     tc_commit<CG>(tfull0 + 8 * acc, pair_mask);   // accumulator ready for the pair's epilogues
                     if (++acc == 2) { acc = 0; aphase ^= 1; }
                 }
+                if constexpr (AR) tc_commit<CG>(aempty, (uint16_t)0x3);   // both CTAs may reload A once these retire
             }
         }
     } else {
@@ -673,6 +711,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1) scree
 }
 
 template <int P, int HC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) screen_tc2a_kernel(SCREEN_TC_ARGS) {
+    screen_tc_body<2, P, HC, 1, TC_EPI_WARPS, 1>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xstat, scal, wcoef,
+                                                 thr0, cand, ccount, flags, dump, sync_ctr, lag, pool, ovf_head,
+                                                 ovf_lim);
+}
+
+template <int P, int HC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) screen_tc2_kernel(SCREEN_TC_ARGS) {
     screen_tc_body<2, P, HC>(&map_x, &map_w, &map_xl, &map_wl, n, dp, kp, c, xstat, scal, wcoef, thr0, cand, ccount,
                              flags, dump, sync_ctr, lag, pool, ovf_head, ovf_lim);
@@ -717,6 +762,8 @@ static int g_tc_group = 2;   // SOMB_TC_GROUP=1 selects the single-CTA variant (
 static int g_half_cap = 32;  // SOMB_HALF_CAP = 8 | 16 | 32: candidates kept per (row, column group)
 static int g_lag = 8;        // SOMB_SCREEN_LAG: soft lockstep of the CTAs' codebook sweeps (0 = off)
 static int g_mc = 2;         // SOMB_TC_MULTICAST: 2 = 4-CTA clusters multicasting the codebook tiles (1-pass screen), 1 = off
+static int g_ares = 1;       // SOMB_A_RESIDENT / knob "a_resident": data-row operands resident per unit (<= 4 K-chunks;
+                             // cfg4 screen 125 -> 107 ms, cfg5 536 -> 510 ms, tools/r2_ar.sh)
 
 template <class KernelT>
 static int set_smem(KernelT k, uint32_t bytes, const char *what) {
@@ -735,6 +782,8 @@ static int screen_tc_init() {
     if (lg) g_lag = atoi(lg);
     const char *mc = getenv("SOMB_TC_MULTICAST");
     if (mc) g_mc = atoi(mc) == 2 ? 2 : 1;
+    const char *ar = getenv("SOMB_A_RESIDENT");
+    if (ar) g_ares = atoi(ar) != 0;
     const char *pm = getenv("SOMB_SCREEN_PROFILE");
     int mode = pm ? atoi(pm) : 0;
     cudaMemcpyToSymbol(g_profile_mode, &mode, sizeof(int));
@@ -750,6 +799,11 @@ static int screen_tc_init() {
     if (!rc) rc = set_smem(screen_tc2_kernel<3, 16>, TcCfg<2, 3, 16>::SMEM, "screen_tc2x3 smem");
     if (!rc) rc = set_smem(screen_tc2_kernel<3, 32>, TcCfg<2, 3, 32>::SMEM, "screen_tc2x3 smem");
     if (!rc) rc = set_smem(screen_tc2_kernel<2, 32>, TcCfg<2, 2, 32>::SMEM, "screen_tc2x2 smem");
+    if (!rc) rc = set_smem(screen_tc2_kernel<2, 16>, TcCfg<2, 2, 16>::SMEM, "screen_tc2x2 smem");
+    if (!rc) rc = set_smem(screen_tc2a_kernel<1, 32>, TcCfg<2, 1, 32, TC_EPI_WARPS, 1>::SMEM, "screen_tc2a smem");
+    if (!rc) rc = set_smem(screen_tc2a_kernel<2, 32>, TcCfg<2, 2, 32, TC_EPI_WARPS, 1>::SMEM, "screen_tc2a smem");
+    if (!rc) rc = set_smem(screen_tc2a_kernel<1, 16>, TcCfg<2, 1, 16, TC_EPI_WARPS, 1>::SMEM, "screen_tc2a smem");
+    if (!rc) rc = set_smem(screen_tc2a_kernel<2, 16>, TcCfg<2, 2, 16, TC_EPI_WARPS, 1>::SMEM, "screen_tc2a smem");
     if (!rc) rc = set_smem(screen_tc4_kernel<1, 32>, TcCfg<2, 1, 32>::SMEM, "screen_tc4 smem");
     if (!rc) rc = set_smem(screen_tc4_kernel<2, 32>, TcCfg<2, 2, 32>::SMEM, "screen_tc4x2 smem");
     if (!rc) rc = set_smem(screen_tc4_kernel<3, 32>, TcCfg<2, 3, 32>::SMEM, "screen_tc4x3 smem");
@@ -766,6 +820,7 @@ int screen_tc_set_knob(const char *key, int value) {
     if (!strcmp(key, "half_cap")) { g_half_cap = value <= 8 ? 8 : value <= 16 ? 16 : 32; return SOMB_OK; }
     if (!strcmp(key, "tc_group")) { g_tc_group = value == 1 ? 1 : 2; return SOMB_OK; }
     if (!strcmp(key, "tc_multicast")) { g_mc = value == 2 ? 2 : 1; return SOMB_OK; }
+    if (!strcmp(key, "a_resident")) { g_ares = value != 0; return SOMB_OK; }
     if (!strcmp(key, "screen_profile")) {
         cudaError_t r = cudaMemcpyToSymbol(g_profile_mode, &value, sizeof(int));
         return r == cudaSuccess ? SOMB_OK : cuda_status(r, "set screen_profile");
@@ -788,7 +843,9 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
     SOMB_REQUIRE(passes >= 1 && passes <= 3 && (passes == 1 || (Xl && Wl)), SOMB_E_INPUT,
                  "screen_tc: %d passes need the split operands", passes);
     const bool three = passes == 3, two = passes == 2;
-    const int mcv = cg == 2 && g_half_cap == 32 && passes == 1 ? g_mc : 1;   // (2-pass with multicast measured slower)
+    const int kchunks = (dp + TC_BK - 1) / TC_BK + (two ? (2 * dp + 127) / 128 : 0);
+    const bool use_ar = g_ares && cg == 2 && !three && kchunks <= 4;   // A-resident (no codebook multicast)
+    const int mcv = cg == 2 && g_half_cap == 32 && passes == 1 && !use_ar ? g_mc : 1;   // (2-pass with multicast measured slower)
     CUtensorMap mx, mw, mxl, mwl;
     int rc = make_map(&mx, Xh, (uint64_t)dp, (uint64_t)n, TC_ROWS);
     if (!rc) rc = make_map(&mw, Wh, (uint64_t)dp, (uint64_t)kp, (uint32_t)(TC_BN / cg / mcv));
@@ -836,9 +893,20 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
     KERN<PV, HV><<<grid, TC_THREADS, TcCfg<CGV, PV, HV>::SMEM, st>>>(mx, mw, mxl, mwl, n, dp, kp, c, xstat, scal, wcoef, \
                                                                      thr0, cand, ccount, flags, dump, ctr, lag, pool, \
                                                                      ovf_head, ovf_lim)
-    if (two) {
+#define SCREEN_LAUNCH_AR(PV, HV)                                                                                    \
+    screen_tc2a_kernel<PV, HV><<<grid, TC_THREADS, TcCfg<2, PV, HV, TC_EPI_WARPS, 1>::SMEM, st>>>(                    \
+        mx, mw, mxl, mwl, n, dp, kp, c, xstat, scal, wcoef, thr0, cand, ccount, flags, dump, ctr, lag, pool, ovf_head, \
+        ovf_lim)
+    if (use_ar) {
+        if (g_half_cap <= 16) {
+            if (two) SCREEN_LAUNCH_AR(2, 16); else SCREEN_LAUNCH_AR(1, 16);
+        } else {
+            if (two) SCREEN_LAUNCH_AR(2, 32); else SCREEN_LAUNCH_AR(1, 32);
+        }
+    } else if (two) {
         SOMB_REQUIRE(cg == 2, SOMB_E_CONFIG, "screen_tc: the fp8 split screen needs CTA pairs (tc_group 2)");
         if (mcv == 2) SCREEN_LAUNCH(screen_tc4_kernel, 2, 2, 32);
+        else if (g_half_cap <= 16) SCREEN_LAUNCH(screen_tc2_kernel, 2, 2, 16);   // smaller lists, one more stage
         else SCREEN_LAUNCH(screen_tc2_kernel, 2, 2, 32);
     } else if (cg == 1) {
         if (three) SCREEN_LAUNCH(screen_tc1_kernel, 1, 3, 16); else SCREEN_LAUNCH(screen_tc1_kernel, 1, 1, 16);
@@ -854,6 +922,7 @@ int launch_screen_tc(const __half *Xh, const __half *Xl, int64_t n, int dp, cons
         else SCREEN_LAUNCH(screen_tc2_kernel, 2, 1, 32);
     }
 #undef SCREEN_LAUNCH
+#undef SCREEN_LAUNCH_AR
     note_launch();
     SOMB_LAUNCH_CHECK("screen_tc");
     return SOMB_OK;

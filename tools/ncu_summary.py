@@ -30,7 +30,7 @@ def main():
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[e["unit"]]
         return float(e["value"].replace(",", "")) * scale
     dram = to_bytes(m["dram__bytes_read.sum"]) + to_bytes(m["dram__bytes_write.sum"])
-    res = {"kernel": kernel, "workload": workload, "capture": cmd, "round": 1, "metrics": m,
+    res = {"kernel": kernel, "workload": workload, "capture": cmd, "round": 2, "metrics": m,
            "dram_bytes_per_launch": dram}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps({"dram_bytes_per_launch": dram, "time": m["gpu__time_duration.sum"]}))
