@@ -251,13 +251,23 @@ SOMB_API int somb_sparse_row_stats(const int64_t *rowptr, const float *val, int6
 SOMB_API int somb_sparse_codebook_T(const float *W, const float *mu, int32_t K, int32_t d,
                                     int32_t kp, float *dT, void *stream);
 /* fp32 gather screen over dT + exact fp64 sparse re-rank (exact = 1: scan
- * every node, no screen).  ws >= somb_bmu_ws(n). */
+ * every node, no screen; exact = 2: screen, and leave the rows whose
+ * candidate set was truncated to somb_bmu_sparse_repair).  ws >= somb_bmu_ws(n). */
 SOMB_API int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const float *val,
                              int64_t n, int32_t d, const float *dT, const float *W,
                              const float *c, const double *w2, int32_t K, int32_t kp,
                              const float *scal, const double *x2, const float *xnorm,
                              float window_coef, int32_t exact, int32_t *bmu,
                              double *d2min, int32_t *flags, void *ws, void *stream);
+/* After somb_bmu_sparse(exact = 2) on the same ws: the exact BMU of every
+ * row whose candidate set was truncated, by a slab-lockstep fp64 scan of all
+ * nodes over WT[k][j] = w_jk (the ORIGINAL codebook transposed, pitch kp:
+ * somb_sparse_codebook_T with mu = 0); the reference's sparse formula
+ * (kernels.py:216-219), first-minimum ties (kernels.py:27-28). */
+SOMB_API int somb_bmu_sparse_repair(const int64_t *rowptr, const int32_t *col, const float *val,
+                                    int64_t n, const float *WT, int32_t K, int32_t kp,
+                                    const double *w2, const double *x2, int32_t *bmu, double *d2min,
+                                    void *ws, void *stream);
 /* S (K x d, fp64, dense) / cnt from CSR rows; ws >= somb_node_sums_ws(n, d, K).
  * Nodes with more than 2048 rows are summed in 2048-row segments folded in
  * segment order (the dense path's scheme), else in ascending row order. */

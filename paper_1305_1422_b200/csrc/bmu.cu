@@ -56,20 +56,24 @@ BmuWs bmu_carve(void *ws, int64_t n, size_t *total) {
 // for every row, truncated or not.  flags: bit 0 of any byte = truncated
 // (one byte per column group of the tcgen05 screen, one word otherwise);
 // ctr counts the repaired rows (ws counter 4, somb_bmu_repaired_rows).
+// The row ids are also listed at list[0, *ctr) when a list is given (the
+// sparse path re-ranks them with a slab-lockstep exact scan, sparse.cu).
 __global__ void repair_truncated_kernel(const int *__restrict__ flags, int *__restrict__ ccount, int64_t n,
-                                        unsigned *__restrict__ ctr) {
+                                        unsigned *__restrict__ ctr, int *__restrict__ list) {
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n) return;
     if (flags[row] & 0x01010101) {
         ccount[row] = kScanAll;
-        atomicAdd(ctr, 1u);
+        const unsigned i = atomicAdd(ctr, 1u);
+        if (list) list[i] = (int)row;
     }
 }
 
-int launch_repair_truncated(const int *flags, int *ccount, int64_t n, unsigned *ctrs, cudaStream_t st) {
+int launch_repair_truncated(const int *flags, int *ccount, int64_t n, unsigned *ctrs, cudaStream_t st,
+                            int *list) {
     cudaMemsetAsync(ctrs + 4, 0, sizeof(unsigned), st);
     if (n == 0) return SOMB_OK;
-    repair_truncated_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flags, ccount, n, ctrs + 4);
+    repair_truncated_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flags, ccount, n, ctrs + 4, list);
     note_launch();
     SOMB_LAUNCH_CHECK("repair_truncated");
     return SOMB_OK;
@@ -735,7 +739,7 @@ extern "C" int somb_bmu_screen(const uint16_t *Xh, const uint16_t *Xl, const flo
         note_launch();
         SOMB_LAUNCH_CHECK("screen_simt");
     }
-    return launch_repair_truncated(flags, ccount, n, w.ctrs, st);
+    return launch_repair_truncated(flags, ccount, n, w.ctrs, st, nullptr);
 }
 
 

@@ -14,7 +14,7 @@
 
 namespace somb {
 
-int launch_repair_truncated(const int *flags, int *ccount, int64_t n, unsigned *ctrs, cudaStream_t st);
+int launch_repair_truncated(const int *flags, int *ccount, int64_t n, unsigned *ctrs, cudaStream_t st, int *list);
 
 constexpr int SP_WARPS = 8;
 constexpr int SP_NNZ_BUF = 256;      // staged (col, val) pairs per warp
@@ -265,9 +265,10 @@ __global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
     const int64_t e0 = rowptr[row], e1 = rowptr[row + 1];
-    int cnt = all ? 0 : ccount[row];
+    int cnt = all == 1 ? 0 : ccount[row];
+    if (all == 2 && cnt < 0) return;   // repaired row: somb_bmu_sparse_repair's lockstep scan takes it
     // repaired row (kScanAll), or no candidate anywhere: exact scan of every node
-    const bool scan = all || cnt < 0 || (cnt == 0 && ovf_head[4 * row] < 0);
+    const bool scan = all == 1 || cnt < 0 || (cnt == 0 && ovf_head[4 * row] < 0);
     if (scan) cnt = K;
     double best = INFINITY;
     int bestj = 0x7fffffff;
@@ -302,6 +303,106 @@ __global__ void sp_rerank_kernel(const int64_t *__restrict__ rowptr, const int *
         bmu[row] = bestj;
         d2min[row] = best;
     }
+}
+
+// Exact scan of the repaired rows (truncated candidate sets), slab-lockstep
+// like the screen: all warps sweep the same 128-node slab of the transposed
+// ORIGINAL codebook WT[k][j] = w_jk (exact copy, pitch kp) before the next,
+// so the slab stays in L2; per (row, node) the reference's sparse formula
+// (x2 - 2 sum_t v_t w_j[col_t]) + w2_j, clamped >= 0 (kernels.py:216-219),
+// with fp32 products accumulated exactly in fp64; first minimum (lowest
+// index) over nodes.  A row's running best lives in its own (unused)
+// candidate slots.  The per-row full scan gathered 250 scattered codebook
+// values per node and took 4 s in cfg3's degenerate epoch 1.
+__global__ void __launch_bounds__(32 * SP_WARPS)
+sp_exact_ls_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col, const float *__restrict__ val,
+                   const int *__restrict__ list, const unsigned *__restrict__ nlist, const float *__restrict__ WT,
+                   int kp, int K, const double *__restrict__ w2, const double *__restrict__ x2,
+                   int *__restrict__ cand, int *__restrict__ bmu, double *__restrict__ d2min,
+                   unsigned *__restrict__ done_ctr) {
+    __shared__ int s_col[SP_WARPS][SP_NNZ_BUF];
+    __shared__ float s_val[SP_WARPS][SP_NNZ_BUF];
+    const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * SP_WARPS + w, GW = (int64_t)gridDim.x * SP_WARPS;
+    const int64_t m = (int64_t)*nlist;
+    if (m == 0) return;
+    auto best_of = [&](int64_t row) { return reinterpret_cast<double *>(cand + row * SOMB_CAND_CAP); };
+    if (lane == 0)
+        for (int64_t i = gw; i < m; i += GW) {
+            const int64_t row = list[i];
+            *best_of(row) = INFINITY;
+            cand[row * SOMB_CAND_CAP + 2] = 0x7fffffff;
+        }
+    const int NC = kp / SPL_CH;
+    for (int ci = 0; ci < NC; ++ci) {
+        if (lane == 0 && ci > 0) {   // slab barrier
+            const unsigned need = (unsigned)GW * (unsigned)ci;
+            for (int spin = 0; spin < (1 << 22); ++spin) {
+                unsigned cur;
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(done_ctr) : "memory");
+                if (cur >= need) break;
+                __nanosleep(128);
+            }
+        }
+        __syncwarp();
+        const int jl = ci * SPL_CH + lane * 4;
+#pragma unroll 1
+        for (int64_t i = gw; i < m; i += GW) {
+            const int64_t row = list[i];
+            const int64_t e0 = rowptr[row], e1 = rowptr[row + 1];
+            const int nnz = (int)(e1 - e0);
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int b0 = 0; b0 < nnz; b0 += SP_NNZ_BUF) {
+                const int mm = min(SP_NNZ_BUF, nnz - b0);
+                __syncwarp();
+                for (int t = lane; t < mm; t += 32) {
+                    s_col[w][t] = col[e0 + b0 + t];
+                    s_val[w][t] = val[e0 + b0 + t];
+                }
+                __syncwarp();
+#pragma unroll 8
+                for (int t = 0; t < mm; ++t) {
+                    const double v = (double)s_val[w][t];
+                    const float4 a = __ldg(reinterpret_cast<const float4 *>(WT + (int64_t)s_col[w][t] * kp + jl));
+                    acc[0] = __fma_rn(v, (double)a.x, acc[0]); acc[1] = __fma_rn(v, (double)a.y, acc[1]);
+                    acc[2] = __fma_rn(v, (double)a.z, acc[2]); acc[3] = __fma_rn(v, (double)a.w, acc[3]);
+                }
+            }
+            const double xx = x2[row];
+            double bv = INFINITY;
+            int bj = 0x7fffffff;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = jl + q;
+                if (j < K) {
+                    const double v = fmax(__dadd_rn(__dsub_rn(xx, __dmul_rn(2.0, acc[q])), w2[j]), 0.0);
+                    if (v < bv) { bv = v; bj = j; }   // ascending j: strict < keeps the first minimum
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+            }
+            if (lane == 0 && bj != 0x7fffffff) {
+                double *bp = best_of(row);
+                int *jp = cand + row * SOMB_CAND_CAP + 2;
+                if (bv < *bp) { *bp = bv; *jp = bj; }   // slabs in ascending node order: earlier wins ties
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(done_ctr, 1u);
+        }
+    }
+    if (lane == 0)
+        for (int64_t i = gw; i < m; i += GW) {
+            const int64_t row = list[i];
+            bmu[row] = cand[row * SOMB_CAND_CAP + 2];
+            d2min[row] = *best_of(row);
+        }
 }
 
 int node_bucket_sort(const int *bmu, int64_t n, int K, void *ws, const int **perm, const int **off, double *cnt,
@@ -386,7 +487,8 @@ extern "C" int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const 
     cudaStream_t st = as_stream(stream);
     BmuWs w = bmu_carve(ws, n);
     int *cand = w.cand, *ccount = w.ccount;
-    if (!exact) {
+    SOMB_REQUIRE(exact >= 0 && exact <= 2, SOMB_E_CONFIG, "bmu_sparse: exact must be 0, 1 or 2");
+    if (exact != 1) {
         cudaMemsetAsync(w.ctrs, 0, 4 * sizeof(unsigned), st);
         static int ls = -1, lag = 0;   // SOMB_SPARSE_LOCKSTEP=0: row-at-a-time gather; SOMB_SPARSE_LAG (0 = slab barrier, measured best)
         if (ls < 0) {
@@ -420,7 +522,8 @@ extern "C" int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const 
                 w.ovf_lim);
         }
         note_launch();
-        int rc = launch_repair_truncated(flags, ccount, n, w.ctrs, st);   // truncated rows -> exact full scan
+        // truncated rows -> exact full scan (listed in the thr0 area for somb_bmu_sparse_repair)
+        int rc = launch_repair_truncated(flags, ccount, n, w.ctrs, st, reinterpret_cast<int *>(w.thr0));
         if (rc) return rc;
     } else {
         cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st);
@@ -429,6 +532,28 @@ extern "C" int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const 
                                                               exact, w.pool, w.ovf_head, w.ovf_lim, bmu, d2min);
     note_launch();
     SOMB_LAUNCH_CHECK("bmu_sparse");
+    return SOMB_OK;
+}
+
+extern "C" int somb_bmu_sparse_repair(const int64_t *rowptr, const int32_t *col, const float *val, int64_t n,
+                                      const float *WT, int32_t K, int32_t kp, const double *w2, const double *x2,
+                                      int32_t *bmu, double *d2min, void *ws, void *stream) {
+    SOMB_REQUIRE(K > 0 && kp % SPL_CH == 0 && kp >= K && WT, SOMB_E_INPUT, "bmu_sparse_repair: bad shape");
+    if (n == 0) return SOMB_OK;
+    cudaStream_t st = as_stream(stream);
+    BmuWs w = bmu_carve(ws, n);
+    cudaMemsetAsync(w.ctrs + 6, 0, sizeof(unsigned), st);
+    int dev = 0, sms = kSmCount, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sp_exact_ls_kernel, 32 * SP_WARPS, 0);
+    if (per_sm < 1) per_sm = 1;
+    // a persistent grid that is always co-resident (the slab barrier waits for every warp)
+    sp_exact_ls_kernel<<<(unsigned)(per_sm * sms), 32 * SP_WARPS, 0, st>>>(
+        rowptr, col, val, reinterpret_cast<const int *>(w.thr0), w.ctrs + 4, WT, kp, K, w2, x2, w.cand, bmu, d2min,
+        w.ctrs + 6);
+    note_launch();
+    SOMB_LAUNCH_CHECK("bmu_sparse_repair");
     return SOMB_OK;
 }
 

@@ -52,6 +52,10 @@ class SparseEngine(SomEngine):
         self.Wh = None
         self.Wl = None
         self.dT = torch.empty((self.d, self.kp), dtype=torch.float32, device=self.dev)
+        # the original codebook transposed (exact copy) for the lockstep repair
+        # scan of truncated rows (somb_bmu_sparse_repair); built per epoch
+        self.WT = torch.empty((self.d, self.kp), dtype=torch.float32, device=self.dev)
+        self._zero_mu = torch.zeros(self.d, dtype=torch.float32, device=self.dev)
 
     def _window_coef(self) -> float:
         return _SPARSE_WINDOW
@@ -64,6 +68,8 @@ class SparseEngine(SomEngine):
         # the codebook mean mu is the first d floats of the prepare workspace
         _lib.call("somb_sparse_codebook_T", _ptr(self.W), _ptr(self.ws), self.K, self.d, self.kp,
                   _ptr(self.dT), st)
+        _lib.call("somb_sparse_codebook_T", _ptr(self.W), _ptr(self._zero_mu), self.K, self.d, self.kp,
+                  _ptr(self.WT), st)
 
     def search(self, dist_mode=_lib.DIST_BLOCKED):
         self._mark("prepare", True)
@@ -75,8 +81,12 @@ class SparseEngine(SomEngine):
         _lib.call("somb_bmu_sparse", _ptr(self.rowptr), _ptr(self.col), _ptr(self.val), self.n, self.d,
                   _ptr(self.dT), _ptr(self.W), _ptr(self.c), _ptr(self.w2), self.K, self.kp,
                   _ptr(self.scal), _ptr(self.x2), _ptr(self.xnorm), C.c_float(self.window_coef),
-                  int(self.screen_impl == 2), _ptr(self.bmu), _ptr(self.d2min), _ptr(self.flags),
+                  1 if self.screen_impl == 2 else 2, _ptr(self.bmu), _ptr(self.d2min), _ptr(self.flags),
                   _ptr(self.ws), _stream(self.dev))
+        if self.screen_impl != 2:   # rows whose candidate set was truncated: exact lockstep scan
+            _lib.call("somb_bmu_sparse_repair", _ptr(self.rowptr), _ptr(self.col), _ptr(self.val), self.n,
+                      _ptr(self.WT), self.K, self.kp, _ptr(self.w2), _ptr(self.x2), _ptr(self.bmu),
+                      _ptr(self.d2min), _ptr(self.ws), _stream(self.dev))
         self._mark("screen", False)
         self.has_prev = True
 
