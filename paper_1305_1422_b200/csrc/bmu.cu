@@ -431,13 +431,17 @@ constexpr int RP_WARPS = 4;      // warps per block
 // pre-scaled by 2^896, exact since |x| < 2^128), splitting the conversions
 // over the XU and integer pipes.
 template <int Q>
-struct PipeSplit { static constexpr int PQA = (3 * Q) / 8; };
+struct PipeSplit { static constexpr int PQA = Q; };
+// (a template parameter of the kernel; round 2 measured the split at cfg2,
+// ~33 candidates per row: all F2F 26.0 ms, 5 of 8 26.3, 4 27.5, 3 (the
+// round-1 choice) 28.6-28.9, 2 30.1, none 34.3 (tools/r2_f2f.sh); all F2F
+// also took cfg4 8.4 -> 6.7 ms and cfg5 22.4 -> 21.7 ms)
 
-template <int Q, int MODE>
+template <int Q, int MODE, int PQ = PipeSplit<Q>::PQA>
 __device__ __forceinline__ void row_operand(const float4 (&x)[Q], double (&xd)[Q][4]) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        const double sc = (MODE != SOMB_DIST_NAIVE && q >= PipeSplit<Q>::PQA) ? kF64Scale : 1.0;
+        const double sc = (MODE != SOMB_DIST_NAIVE && q >= PQ) ? kF64Scale : 1.0;
         xd[q][0] = (double)x[q].x * sc; xd[q][1] = (double)x[q].y * sc;
         xd[q][2] = (double)x[q].z * sc; xd[q][3] = (double)x[q].w * sc;
     }
@@ -445,7 +449,7 @@ __device__ __forceinline__ void row_operand(const float4 (&x)[Q], double (&xd)[Q
 
 // Eight independent accumulators (component x slice parity); fixed pairwise
 // combination order, so the result is deterministic.
-template <int Q, int MODE>
+template <int Q, int MODE, int PQ = PipeSplit<Q>::PQA>
 __device__ __forceinline__ double dist_part_mixed(const double (&x)[Q][4], const float4 (&w)[Q]) {
     double s[8];
 #pragma unroll
@@ -456,7 +460,7 @@ __device__ __forceinline__ double dist_part_mixed(const double (&x)[Q][4], const
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             double &acc = s[(q & 1) * 4 + c];
-            if (q < PipeSplit<Q>::PQA) {
+            if (q < PQ) {
                 const double wd = (double)wf[c];
                 if (MODE == SOMB_DIST_NAIVE) {
                     const double a = wd - x[q][c];
@@ -479,7 +483,7 @@ __device__ __forceinline__ double dist_part_mixed(const double (&x)[Q][4], const
                      __dadd_rn(__dadd_rn(s[2], s[6]), __dadd_rn(s[3], s[7])));
 }
 
-template <int Q, int MODE>
+template <int Q, int MODE, int PQ = PipeSplit<Q>::PQA>
 __global__ void __launch_bounds__(32 * RP_WARPS, 3)
 rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, int64_t n, int d,
                    const float *__restrict__ W, const double *__restrict__ w2, int K,
@@ -511,7 +515,7 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
     {
         float4 xv[Q];
         load_row4<Q>(X, row, d4, lane, xv);
-        row_operand<Q, MODE>(xv, xd);
+        row_operand<Q, MODE, PQ>(xv, xd);
     }
     const int cc = ccount[row];
     const CandLayout L = cand_layout(cc, split, split && ov.ngp ? (int)*ov.ngp : 2);
@@ -597,7 +601,7 @@ rerank_pipe_kernel(const float *__restrict__ X, const double *__restrict__ x2, i
                     for (int t = 0; t < Q; ++t) wv[t] = ring[wib][stg][t][lane];
                     if (jn >= 0) issue(jn, stg);
                     cp_async_commit();
-                    p[i] = dist_part_mixed<Q, MODE>(xd, wv);
+                    p[i] = dist_part_mixed<Q, MODE, PQ>(xd, wv);
                 }
             }
             consider4(p, jg);
