@@ -434,7 +434,7 @@ template <int Q>
 struct PipeSplit { static constexpr int PQA = Q; };
 // (a template parameter of the kernel; round 2 measured the split at cfg2,
 // ~33 candidates per row: all F2F 26.0 ms, 5 of 8 26.3, 4 27.5, 3 (the
-// round-1 choice) 28.6-28.9, 2 30.1, none 34.3 (tools/r2_f2f.sh); all F2F
+// round-1 choice) 28.6-28.9, 2 30.1, none 34.3 (per-split builds); all F2F
 // also took cfg4 8.4 -> 6.7 ms and cfg5 22.4 -> 21.7 ms)
 
 template <int Q, int MODE, int PQ = PipeSplit<Q>::PQA>
