@@ -409,6 +409,16 @@ def run_ours(args):
         roofline["tmem_read"] = {"bytes_per_launch": tm_bytes, "achieved": tm_gbs, "peak": tm_peak, "unit": "GB/s",
                                  "frac": tm_gbs / tm_peak,
                                  "peak_kind": "148 SMs x 64 B/clk (tcgen05.ld throughput) x max SM clock"}
+        # serial floor: the tile's MMAs at the measured burst tensor rate PLUS
+        # its accumulator reads at the TMEM read rate (outstanding tcgen05.ld
+        # was measured to stall the MMAs: the two do not overlap)
+        burst = pk.get("bf16_tflops", peak_sus)
+        t_mma = flops * passes / (burst * 1e12)
+        t_tm = tm_bytes / (tm_peak * 1e9)
+        roofline["mma_plus_tmem_floor"] = {"floor_ms": (t_mma + t_tm) * 1e3, "mma_ms": t_mma * 1e3,
+                                           "tmem_read_ms": t_tm * 1e3, "frac": (t_mma + t_tm) * 1e3 / scr_ms,
+                                           "note": "executed tensor work at the measured burst bf16 rate plus "
+                                                   "4*n*kp accumulator bytes at 64 B/clk/SM, serialised"}
     if sparse:
         simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12
         gflops = 2.0 * count * SPARSE_NNZ * K / (scr_ms / 1e3) / 1e12
