@@ -261,13 +261,14 @@ SOMB_API int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const fl
                              double *d2min, int32_t *flags, void *ws, void *stream);
 /* After somb_bmu_sparse(exact = 2) on the same ws: the exact BMU of every
  * row whose candidate set was truncated, by a slab-lockstep fp64 scan of all
- * nodes over WT[k][j] = w_jk (the ORIGINAL codebook transposed, pitch kp:
- * somb_sparse_codebook_T with mu = 0); the reference's sparse formula
- * (kernels.py:216-219), first-minimum ties (kernels.py:27-28). */
+ * nodes over the ORIGINAL codebook transposed into `WT` (d x kp f32 scratch,
+ * e.g. the screen's dT buffer once the screen is done; written only when a
+ * row was repaired); the reference's sparse formula (kernels.py:216-219),
+ * first-minimum ties (kernels.py:27-28). */
 SOMB_API int somb_bmu_sparse_repair(const int64_t *rowptr, const int32_t *col, const float *val,
-                                    int64_t n, const float *WT, int32_t K, int32_t kp,
-                                    const double *w2, const double *x2, int32_t *bmu, double *d2min,
-                                    void *ws, void *stream);
+                                    int64_t n, int32_t d, const float *W, int32_t K, int32_t kp,
+                                    const double *w2, const double *x2, float *WT, int32_t *bmu,
+                                    double *d2min, void *ws, void *stream);
 /* S (K x d, fp64, dense) / cnt from CSR rows; ws >= somb_node_sums_ws(n, d, K).
  * Nodes with more than 2048 rows are summed in 2048-row segments folded in
  * segment order (the dense path's scheme), else in ascending row order. */

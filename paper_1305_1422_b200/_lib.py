@@ -84,7 +84,7 @@ SIGNATURES = {
     "somb_bmu_sparse": (C.c_int, [P, P, P, I64, I32, P, P, P, P, I32, I32, P, P, P, F32, I32,
                                   P, P, P, P, P]),
     "somb_bmu_sparse_ws": (SZ, [I64]),
-    "somb_bmu_sparse_repair": (C.c_int, [P, P, P, I64, P, I32, I32, P, P, P, P, P, P]),
+    "somb_bmu_sparse_repair": (C.c_int, [P, P, P, I64, I32, P, I32, I32, P, P, P, P, P, P, P]),
     "somb_node_sums_sparse": (C.c_int, [P, P, P, I64, I32, P, I32, P, P, P, P, P]),
     "somb_umatrix": (C.c_int, [P, I32, C.POINTER(SombMap), P, P]),
 }

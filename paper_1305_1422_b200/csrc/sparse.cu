@@ -37,6 +37,26 @@ __global__ void sp_transpose(const float *__restrict__ W, const float *__restric
     }
 }
 
+// WT[k][j] = w_jk exactly (the repair scan's operand), only when rows were
+// repaired (*nlist > 0): written into the caller's dT buffer after the screen
+// has used it (the next prepare rebuilds dT)
+__global__ void sp_transpose_if(const float *__restrict__ W, int K, int d, int kp, float *__restrict__ WT,
+                                const unsigned *__restrict__ nlist) {
+    if (*nlist == 0) return;
+    __shared__ float tile[32][33];
+    const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+    for (int r = ty; r < 32; r += 8) {
+        int j = j0 + r, k = k0 + tx;
+        tile[r][tx] = (j < K && k < d) ? W[(int64_t)j * d + k] : 0.0f;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        int k = k0 + r, j = j0 + tx;
+        if (k < d && j < kp) WT[(int64_t)k * kp + j] = tile[tx][r];
+    }
+}
+
 __global__ void sp_row_norms(const int64_t *__restrict__ rowptr, const float *__restrict__ val, int64_t n,
                              double *__restrict__ x2, float *__restrict__ xnorm, int *__restrict__ nnz_max) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -536,12 +556,16 @@ extern "C" int somb_bmu_sparse(const int64_t *rowptr, const int32_t *col, const 
 }
 
 extern "C" int somb_bmu_sparse_repair(const int64_t *rowptr, const int32_t *col, const float *val, int64_t n,
-                                      const float *WT, int32_t K, int32_t kp, const double *w2, const double *x2,
-                                      int32_t *bmu, double *d2min, void *ws, void *stream) {
-    SOMB_REQUIRE(K > 0 && kp % SPL_CH == 0 && kp >= K && WT, SOMB_E_INPUT, "bmu_sparse_repair: bad shape");
+                                      int32_t d, const float *W, int32_t K, int32_t kp, const double *w2,
+                                      const double *x2, float *WT, int32_t *bmu, double *d2min, void *ws,
+                                      void *stream) {
+    SOMB_REQUIRE(K > 0 && d > 0 && kp % SPL_CH == 0 && kp >= K && W && WT, SOMB_E_INPUT,
+                 "bmu_sparse_repair: bad shape");
     if (n == 0) return SOMB_OK;
     cudaStream_t st = as_stream(stream);
     BmuWs w = bmu_carve(ws, n);
+    sp_transpose_if<<<dim3((kp + 31) / 32, (d + 31) / 32), dim3(32, 8), 0, st>>>(W, K, d, kp, WT, w.ctrs + 4);
+    note_launch();
     cudaMemsetAsync(w.ctrs + 6, 0, sizeof(unsigned), st);
     int dev = 0, sms = kSmCount, per_sm = 1;
     cudaGetDevice(&dev);

@@ -51,11 +51,10 @@ class SparseEngine(SomEngine):
     def _init_codebook_buffers(self):
         self.Wh = None
         self.Wl = None
+        # the centred codebook transposed (the gather screen); after the screen
+        # the repair of truncated rows reuses it for the ORIGINAL codebook
+        # transposed (somb_bmu_sparse_repair), and the next prepare rebuilds it
         self.dT = torch.empty((self.d, self.kp), dtype=torch.float32, device=self.dev)
-        # the original codebook transposed (exact copy) for the lockstep repair
-        # scan of truncated rows (somb_bmu_sparse_repair); built per epoch
-        self.WT = torch.empty((self.d, self.kp), dtype=torch.float32, device=self.dev)
-        self._zero_mu = torch.zeros(self.d, dtype=torch.float32, device=self.dev)
 
     def _window_coef(self) -> float:
         return _SPARSE_WINDOW
@@ -68,8 +67,6 @@ class SparseEngine(SomEngine):
         # the codebook mean mu is the first d floats of the prepare workspace
         _lib.call("somb_sparse_codebook_T", _ptr(self.W), _ptr(self.ws), self.K, self.d, self.kp,
                   _ptr(self.dT), st)
-        _lib.call("somb_sparse_codebook_T", _ptr(self.W), _ptr(self._zero_mu), self.K, self.d, self.kp,
-                  _ptr(self.WT), st)
 
     def search(self, dist_mode=_lib.DIST_BLOCKED):
         self._mark("prepare", True)
@@ -85,8 +82,8 @@ class SparseEngine(SomEngine):
                   _ptr(self.ws), _stream(self.dev))
         if self.screen_impl != 2:   # rows whose candidate set was truncated: exact lockstep scan
             _lib.call("somb_bmu_sparse_repair", _ptr(self.rowptr), _ptr(self.col), _ptr(self.val), self.n,
-                      _ptr(self.WT), self.K, self.kp, _ptr(self.w2), _ptr(self.x2), _ptr(self.bmu),
-                      _ptr(self.d2min), _ptr(self.ws), _stream(self.dev))
+                      self.d, _ptr(self.W), self.K, self.kp, _ptr(self.w2), _ptr(self.x2), _ptr(self.dT),
+                      _ptr(self.bmu), _ptr(self.d2min), _ptr(self.ws), _stream(self.dev))
         self._mark("screen", False)
         self.has_prev = True
 
