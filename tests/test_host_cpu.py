@@ -286,3 +286,44 @@ def test_bindings_sparse_branch_validation(tmp_path):
         B.train_wrapper(str(dn), 1, 3, 2, 3, 2, 0, 0, "linear", 0, 0, "linear", 0, 2, "planar", "", cb, bm, um)
     with pytest.raises(B.ShapeError):
         B.train_wrapper(str(sp), 1, 3, 2, 3, 3, 0, 0, "linear", 0, 0, "linear", 0, 2, "planar", "", cb, bm, um)
+
+
+@pytest.mark.parametrize("nbh,compact", [("gaussian", False), ("gaussian", True), ("bubble", False), ("bubble", True)])
+@pytest.mark.parametrize("mt", ["planar", "toroid"])
+def test_hex_epoch_vs_brute_force(nbh, compact, mt):
+    """The extension's whole epoch (hex lattice x bubble / compact support) in
+    the oracle against a brute-force restatement written the slow obvious way,
+    like the reference's epoch_brute (tests/oracles.py:41-79, used by
+    test_acceptance.py:87-118): BMU by a full fp64 scan with first-minimum
+    ties, then for every (row, node) pair h from the 9-image hex distance,
+    num += h x, den += h.  Pins the oracle's extension semantics (the GPU
+    update is checked against the oracle, test_gpu_parity.py)."""
+    import math
+    rng = np.random.default_rng(11)
+    nx, ny, n, d = 6, 4, 60, 3
+    x = rng.random((n, d), dtype=np.float32)
+    w = rng.random((nx * ny, d), dtype=np.float32)
+    radius, cutoff = 1.7, 1e-3
+    tor = mt == "toroid"
+    ob, _, num, den = O.search_accumulate(x, w, nx, ny, radius, cutoff, mt, O.DENSE_BLOCKED, grid=O.HEX,
+                                          neighborhood=nbh, compact=compact)
+    bnum = np.zeros((nx * ny, d))
+    bden = np.zeros(nx * ny)
+    for i in range(n):
+        d2 = [float(np.sum((x[i].astype(np.float64) - w[j].astype(np.float64)) ** 2)) for j in range(nx * ny)]
+        b = min(range(nx * ny), key=lambda j: (d2[j], j))
+        for j in range(nx * ny):
+            dist = _hex_brute(b % nx, b // nx, j % nx, j // nx, nx, ny, tor)
+            if nbh == "bubble":
+                h = 1.0 if dist <= radius else 0.0
+            else:
+                h = math.exp(dist / -radius)
+                if compact and dist > radius:
+                    h = 0.0
+            if h < cutoff:
+                h = 0.0
+            bnum[j] += h * x[i].astype(np.float64)
+            bden[j] += h
+        assert ob[i] == b or abs(d2[ob[i]] - d2[b]) <= 1e-12 * d2[b]
+    np.testing.assert_allclose(num, bnum, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(den, bden, rtol=1e-12, atol=1e-12)
