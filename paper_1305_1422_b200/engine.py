@@ -431,9 +431,11 @@ class SomEngine:
             # rows truncate and are repaired by full scans (exact, but slow:
             # cfg4 near-constant rows, 50% of the rows per epoch).  Then the
             # fp16 + fp8 split screen takes over for the rest of the training.
-            # One 4-byte host read per epoch.
+            # Also when the sets stay complete but large: more spilled
+            # 32-entry chunks than half the rows (uniform cfg4 data spills
+            # ~0.05 per row).  Two 4-byte host reads per epoch.
             rep = self.repaired_rows()
-            if rep > 0.005 * self.n:
+            if rep > 0.005 * self.n or self.overflow_chunks() > self.n // 2:
                 self._switch_to_split()
 
     _adaptive = False
