@@ -217,6 +217,14 @@ SOMB_API size_t somb_node_sums_ws(int64_t n, int32_t d, int32_t K);
 SOMB_API int somb_node_sums_dense(const float *X, int64_t n, int32_t d,
                          const int32_t *bmu, int32_t K, double *S, double *cnt,
                          int32_t *row_order, void *ws, void *stream);
+/* The same sums written column-block-major: S is [ceil(d/dc)][K][dc] fp64,
+ * S[(k / dc)][b][k % dc] = S_bk (padding columns of the last block are 0),
+ * 1 <= dc <= d.  With dc = ceil(d/P) rank r's feature-column block is one
+ * contiguous [K][dc] slab: the multi-rank exchange reduce-scatters S in place
+ * (replaces the MPI_Reduce of the numerators, distributed.py:492-514). */
+SOMB_API int somb_node_sums_dense_cols(const float *X, int64_t n, int32_t d,
+                                      const int32_t *bmu, int32_t K, int32_t dc, double *S,
+                                      double *cnt, int32_t *row_order, void *ws, void *stream);
 
 /* ---- batch update: neighbourhood convolution + blend ------------------
  * h(b, j) from grid offsets (kernels.py:99-150; hex/bubble/compact are
@@ -279,6 +287,11 @@ SOMB_API int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col,
                                    const float *val, int64_t n, int32_t d,
                                    const int32_t *bmu, int32_t K, double *S,
                                    double *cnt, int32_t *row_order, void *ws, void *stream);
+/* Column-block-major S as somb_node_sums_dense_cols. */
+SOMB_API int somb_node_sums_sparse_cols(const int64_t *rowptr, const int32_t *col,
+                                       const float *val, int64_t n, int32_t d,
+                                       const int32_t *bmu, int32_t K, int32_t dc, double *S,
+                                       double *cnt, int32_t *row_order, void *ws, void *stream);
 
 /* Number of kernels this library has launched (process lifetime). */
 SOMB_API unsigned long long somb_launch_count(void);

@@ -75,6 +75,7 @@ SIGNATURES = {
     "somb_set_knob": (C.c_int, [C.c_char_p, I32]),
     "somb_node_sums_ws": (SZ, [I64, I32, I32]),
     "somb_node_sums_dense": (C.c_int, [P, I64, I32, P, I32, P, P, P, P, P]),
+    "somb_node_sums_dense_cols": (C.c_int, [P, I64, I32, P, I32, I32, P, P, P, P, P]),
     "somb_hood_ws": (SZ, [C.POINTER(SombMap), I32, I32]),
     "somb_hood_update": (C.c_int, [P, P, I32, C.POINTER(SombMap), C.POINTER(SombHood), F64, P,
                                    P, I32, I32, P, P, P, P, P]),
@@ -86,6 +87,7 @@ SIGNATURES = {
     "somb_bmu_sparse_ws": (SZ, [I64]),
     "somb_bmu_sparse_repair": (C.c_int, [P, P, P, I64, I32, P, I32, I32, P, P, P, P, P, P, P]),
     "somb_node_sums_sparse": (C.c_int, [P, P, P, I64, I32, P, I32, P, P, P, P, P]),
+    "somb_node_sums_sparse_cols": (C.c_int, [P, P, P, I64, I32, P, I32, I32, P, P, P, P, P]),
     "somb_umatrix": (C.c_int, [P, I32, C.POINTER(SombMap), P, P]),
 }
 

@@ -60,6 +60,15 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
+// Node sums S in column-block-major layout [ceil(d/dc)][K][dc] (dc = d: the
+// plain row-major [K][d]): each rank's feature-column block of S is
+// contiguous, so the multi-rank reduce-scatter reads S in place.
+__host__ __device__ __forceinline__ int64_t s_index(int b, int k, int dc, int K) {
+    const int blk = k / dc;
+    return ((int64_t)blk * K + b) * dc + (k - blk * dc);
+}
+inline size_t s_blocks_size(int d, int dc, int K) { return (size_t)((d + dc - 1) / dc) * K * dc; }
+
 // ---------------------------------------------------------------- grid
 // Node j sits at (col, row) = (j % nx, j / nx) (kernels.py:89-96).
 // Squared grid distance between two nodes, exact in fp64:

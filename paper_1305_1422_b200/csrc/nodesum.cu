@@ -141,12 +141,13 @@ __global__ void seg_plan(const int *__restrict__ cnt, int K, int *__restrict__ n
     if (cnt_out) cnt_out[b] = (double)c;
 }
 
-// One block per 256-row segment of one node: fixed-order fp64 sum.
+// One block per 256-row segment of one node: fixed-order fp64 sum.  S is
+// written column-block-major (s_index, common.cuh): [ceil(d/dc)][K][dc].
 template <int R>
 __global__ void __launch_bounds__(128)
 seg_sum(const float *__restrict__ X, int d, const int *__restrict__ perm, const int *__restrict__ off,
         const int *__restrict__ seg_off, const int *__restrict__ mseg_off, const int *__restrict__ nseg,
-        int K, double *__restrict__ S, double *__restrict__ P) {
+        int K, int dc, double *__restrict__ S, double *__restrict__ P) {
     const int s = blockIdx.x;
     const int total = seg_off[K];
     if (s >= total) return;
@@ -161,7 +162,7 @@ seg_sum(const float *__restrict__ X, int d, const int *__restrict__ perm, const 
     const int sub = s - seg_off[b];
     const int r0 = off[b] + sub * kSeg;
     const int r1 = min(off[b + 1], r0 + kSeg);
-    double *dst = nseg[b] > 1 ? P + (int64_t)(mseg_off[b] + sub) * d : S + (int64_t)b * d;
+    double *prow = nseg[b] > 1 ? P + (int64_t)(mseg_off[b] + sub) * d : nullptr;
     for (int k0 = 0; k0 < d; k0 += 128 * R) {
         double acc[R];
 #pragma unroll
@@ -194,13 +195,16 @@ seg_sum(const float *__restrict__ X, int d, const int *__restrict__ perm, const 
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             int k = k0 + q * 128 + threadIdx.x;
-            if (k < d) dst[k] = acc[q];
+            if (k < d) {
+                if (prow) prow[k] = acc[q];
+                else S[s_index(b, k, dc, K)] = acc[q];
+            }
         }
     }
 }
 
 __global__ void seg_fold(const double *__restrict__ P, const int *__restrict__ mseg_off,
-                         const int *__restrict__ nseg, int d, double *__restrict__ S) {
+                         const int *__restrict__ nseg, int d, int K, int dc, double *__restrict__ S) {
     const int b = blockIdx.x;
     const int ns = nseg[b];
     if (ns <= 1) return;
@@ -208,7 +212,7 @@ __global__ void seg_fold(const double *__restrict__ P, const int *__restrict__ m
     for (int k = threadIdx.x; k < d; k += blockDim.x) {
         double a = 0.0;
         for (int s = 0; s < ns; ++s) a += p[(int64_t)s * d + k];
-        S[(int64_t)b * d + k] = a;
+        S[s_index(b, k, dc, K)] = a;
     }
 }
 
@@ -298,11 +302,18 @@ int node_bucket_sort(const int *bmu, int64_t n, int K, void *ws, const int **per
 
 extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const int32_t *bmu, int32_t K,
                                     double *S, double *cnt, int32_t *row_order, void *ws, void *stream) {
+    return somb_node_sums_dense_cols(X, n, d, bmu, K, d, S, cnt, row_order, ws, stream);
+}
+
+extern "C" int somb_node_sums_dense_cols(const float *X, int64_t n, int32_t d, const int32_t *bmu, int32_t K,
+                                         int32_t dc, double *S, double *cnt, int32_t *row_order, void *ws,
+                                         void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0 && n >= 0 && n < (1ll << 31), SOMB_E_INPUT,
                  "node_sums: bad shape n=%lld d=%d K=%d", (long long)n, d, K);
+    SOMB_REQUIRE(dc > 0 && dc <= d, SOMB_E_INPUT, "node_sums: column block %d outside [1, d=%d]", dc, d);
     cudaStream_t st = as_stream(stream);
     NodeSumWs w = carve(ws, n, d, K);
-    cudaMemsetAsync(S, 0, (size_t)K * d * sizeof(double), st);
+    cudaMemsetAsync(S, 0, s_blocks_size(d, dc, K) * sizeof(double), st);
     const int *perm = nullptr, *off = nullptr;
     int rc = node_bucket_sort(bmu, n, K, ws, &perm, &off, cnt, st);
     if (rc || n == 0) return rc;
@@ -313,13 +324,13 @@ extern "C" int somb_node_sums_dense(const float *X, int64_t n, int32_t d, const 
     note_launch();
     unsigned maxseg = (unsigned)(K + (n + kSeg - 1) / kSeg);
     if (d <= 128)
-        seg_sum<1><<<maxseg, 128, 0, st>>>(X, d, perm, off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
+        seg_sum<1><<<maxseg, 128, 0, st>>>(X, d, perm, off, w.segoff, w.msegoff, w.nseg, K, dc, S, w.P);
     else if (d <= 512)
-        seg_sum<4><<<maxseg, 128, 0, st>>>(X, d, perm, off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
+        seg_sum<4><<<maxseg, 128, 0, st>>>(X, d, perm, off, w.segoff, w.msegoff, w.nseg, K, dc, S, w.P);
     else
-        seg_sum<8><<<maxseg, 128, 0, st>>>(X, d, perm, off, w.segoff, w.msegoff, w.nseg, K, S, w.P);
+        seg_sum<8><<<maxseg, 128, 0, st>>>(X, d, perm, off, w.segoff, w.msegoff, w.nseg, K, dc, S, w.P);
     note_launch();
-    seg_fold<<<K, 128, 0, st>>>(w.P, w.msegoff, w.nseg, d, S);
+    seg_fold<<<K, 128, 0, st>>>(w.P, w.msegoff, w.nseg, d, K, dc, S);
     note_launch();
     SOMB_LAUNCH_CHECK("node_sums");
     return SOMB_OK;

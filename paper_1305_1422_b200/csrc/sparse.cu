@@ -439,7 +439,7 @@ constexpr int SP_SEG = 2048;
 __global__ void sp_seg_sum_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ col,
                                   const float *__restrict__ val, int d, const int *__restrict__ perm,
                                   const int *__restrict__ off, const int *__restrict__ segoff,
-                                  const int *__restrict__ msegoff, const int *__restrict__ nseg, int K,
+                                  const int *__restrict__ msegoff, const int *__restrict__ nseg, int K, int dc,
                                   double *__restrict__ S, double *__restrict__ P) {
     const int s = blockIdx.x;
     if (s >= segoff[K]) return;
@@ -452,16 +452,19 @@ __global__ void sp_seg_sum_kernel(const int64_t *__restrict__ rowptr, const int 
     while (b + 1 <= K && segoff[b + 1] <= s) ++b;
     const int sub = s - segoff[b];
     const int r0 = off[b] + sub * SP_SEG, r1 = min(off[b + 1], r0 + SP_SEG);
-    double *dst = nseg[b] > 1 ? P + (int64_t)(msegoff[b] + sub) * d : S + (int64_t)b * d;
+    double *prow = nseg[b] > 1 ? P + (int64_t)(msegoff[b] + sub) * d : nullptr;
     for (int t = r0; t < r1; ++t) {
         const int i = perm[t];
-        for (int64_t e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x) dst[col[e]] += (double)val[e];
+        for (int64_t e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x) {
+            if (prow) prow[col[e]] += (double)val[e];
+            else S[s_index(b, col[e], dc, K)] += (double)val[e];
+        }
         __syncthreads();
     }
 }
 
 __global__ void sp_seg_fold(const double *__restrict__ P, const int *__restrict__ msegoff,
-                            const int *__restrict__ nseg, int d, double *__restrict__ S) {
+                            const int *__restrict__ nseg, int d, int K, int dc, double *__restrict__ S) {
     const int b = blockIdx.y;
     const int ns = nseg[b];
     if (ns <= 1) return;
@@ -469,7 +472,7 @@ __global__ void sp_seg_fold(const double *__restrict__ P, const int *__restrict_
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < d; k += gridDim.x * blockDim.x) {
         double a = 0.0;
         for (int q = 0; q < ns; ++q) a += p[(int64_t)q * d + k];
-        S[(int64_t)b * d + k] = a;
+        S[s_index(b, k, dc, K)] = a;
     }
 }
 
@@ -584,9 +587,16 @@ extern "C" int somb_bmu_sparse_repair(const int64_t *rowptr, const int32_t *col,
 extern "C" int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col, const float *val, int64_t n,
                                      int32_t d, const int32_t *bmu, int32_t K, double *S, double *cnt,
                                      int32_t *row_order, void *ws, void *stream) {
+    return somb_node_sums_sparse_cols(rowptr, col, val, n, d, bmu, K, d, S, cnt, row_order, ws, stream);
+}
+
+extern "C" int somb_node_sums_sparse_cols(const int64_t *rowptr, const int32_t *col, const float *val, int64_t n,
+                                          int32_t d, const int32_t *bmu, int32_t K, int32_t dc, double *S,
+                                          double *cnt, int32_t *row_order, void *ws, void *stream) {
     SOMB_REQUIRE(K > 0 && d > 0 && n < (1ll << 31), SOMB_E_INPUT, "node_sums_sparse: bad shape");
+    SOMB_REQUIRE(dc > 0 && dc <= d, SOMB_E_INPUT, "node_sums_sparse: column block %d outside [1, d=%d]", dc, d);
     cudaStream_t st = as_stream(stream);
-    cudaMemsetAsync(S, 0, (size_t)K * d * sizeof(double), st);
+    cudaMemsetAsync(S, 0, s_blocks_size(d, dc, K) * sizeof(double), st);
     const int *perm = nullptr, *off = nullptr;
     int rc = node_bucket_sort(bmu, n, K, ws, &perm, &off, cnt, st);
     if (rc) return rc;
@@ -599,9 +609,9 @@ extern "C" int somb_node_sums_sparse(const int64_t *rowptr, const int32_t *col, 
     const size_t need = ((size_t)(n + SP_SEG - 1) / SP_SEG * 2 + 2) * (size_t)d;
     cudaMemsetAsync(P, 0, (need < P_doubles ? need : P_doubles) * sizeof(double), st);
     const unsigned maxseg = (unsigned)(K + (n + SP_SEG - 1) / SP_SEG);
-    sp_seg_sum_kernel<<<maxseg, 256, 0, st>>>(rowptr, col, val, d, perm, off, segoff, msegoff, nseg, K, S, P);
+    sp_seg_sum_kernel<<<maxseg, 256, 0, st>>>(rowptr, col, val, d, perm, off, segoff, msegoff, nseg, K, dc, S, P);
     note_launch();
-    sp_seg_fold<<<dim3((d + 255) / 256 < 64 ? (d + 255) / 256 : 64, K), 256, 0, st>>>(P, msegoff, nseg, d, S);
+    sp_seg_fold<<<dim3((d + 255) / 256 < 64 ? (d + 255) / 256 : 64, K), 256, 0, st>>>(P, msegoff, nseg, d, K, dc, S);
     note_launch();
     SOMB_LAUNCH_CHECK("node_sums_sparse");
     return SOMB_OK;

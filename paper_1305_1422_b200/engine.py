@@ -243,11 +243,19 @@ class SomEngine:
         # in this order so concurrently re-ranked rows share codebook rows in L2
         self.row_order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         self.has_order = False
-        # packed [S (K*d) | cnt (K) | qe (1)] fp64: one all-reduce per epoch
-        self.acc = torch.zeros(self.K * d + self.K + 1, dtype=f64, device=dev)
-        self.S = self.acc[: self.K * d].view(self.K, d)
-        self.cnt = self.acc[self.K * d: self.K * d + self.K]
-        self.qe = self.acc[self.K * d + self.K:]
+        # packed [S | cnt (K) | qe (1)] fp64.  S is [K, d], or with the
+        # column-sharded exchange column-block-major [P, K, dc] (dc = ceil(d/P),
+        # blocks past the last column stay zero): the node-sum kernels write
+        # each rank's column block contiguously, so S is reduce-scattered in
+        # place, without a restaging copy
+        self.cols = self.sharded and self.opt.shard_update == "columns"
+        self.dc = -(-d // self.world) if self.cols else d
+        ssz = self.world * self.K * self.dc if self.cols else self.K * d
+        self.acc = torch.zeros(ssz + self.K + 1, dtype=f64, device=dev)
+        self.S = (self.acc[:ssz].view(self.world, self.K, self.dc) if self.cols
+                  else self.acc[:ssz].view(self.K, d))
+        self.cnt = self.acc[ssz: ssz + self.K]
+        self.qe = self.acc[ssz + self.K:]
         self.dist_tab = None
         if self.opt.hypot_table and grid is GridType.RECTANGULAR:
             self.dist_tab = torch.from_numpy(distance_table(self.nx, self.ny, map_type)).to(dev)
@@ -486,16 +494,14 @@ class SomEngine:
                   _stream(self.dev))
 
     def node_sums(self):
-        _lib.call("somb_node_sums_dense", _ptr(self.X), self.n, self.d, _ptr(self.bmu), self.K,
+        _lib.call("somb_node_sums_dense_cols", _ptr(self.X), self.n, self.d, _ptr(self.bmu), self.K, self.dc,
                   _ptr(self.S), _ptr(self.cnt), _ptr(self.row_order), _ptr(self.ws), _stream(self.dev))
         self.has_order = True
 
     def _col_buffers(self):
         """Staging for the column-sharded exchange (allocated on first use)."""
         if getattr(self, "_Sr", None) is None:
-            dc, K, P, dev = -(-self.d // self.world), self.K, self.world, self.dev
-            self.dc = dc
-            self._Sst = torch.empty((P, K, dc), dtype=torch.float64, device=dev)
+            dc, K, P, dev = self.dc, self.K, self.world, self.dev
             self._Sr = torch.empty((K, dc), dtype=torch.float64, device=dev)
             self._Wst = torch.empty((P, K, dc), dtype=torch.float32, device=dev)
             self._Wold = torch.zeros((K, dc), dtype=torch.float32, device=dev)
@@ -503,13 +509,13 @@ class SomEngine:
 
     def reduce(self):
         if self.sharded:
-            from .parallel import allreduce_sum, reduce_scatter_columns
-            if self.opt.shard_update == "columns":
+            from .parallel import allreduce_sum, reduce_scatter_blocks
+            if self.cols:
                 # this rank's feature columns of S, summed over ranks; the
                 # counts and qe (the contiguous tail of acc) on every rank
                 self._col_buffers()
-                reduce_scatter_columns(self.S, self.dc, self._Sst, self._Sr, self.group)
-                allreduce_sum(self.acc[self.K * self.d:], self.group)
+                reduce_scatter_blocks(self.S, self._Sr, self.group)
+                allreduce_sum(self.acc[self.S.numel():], self.group)
             else:
                 allreduce_sum(self.acc, self.group)
 
@@ -518,7 +524,7 @@ class SomEngine:
         hood = _lib.SombHood(_lib.NBH_BUBBLE if neighborhood is Neighborhood.BUBBLE
                              else _lib.NBH_GAUSSIAN, int(bool(compact)), float(radius), float(cutoff),
                              {"auto": 0, "direct": 1, "spectral": 2}[self.opt.conv], 0)
-        if self.sharded and not all_nodes and self.opt.shard_update == "columns":
+        if self.cols and not all_nodes:
             # all nodes, this rank's columns: the update is independent per
             # feature column, so each column is computed exactly as on one GPU
             from .parallel import allgather_columns
@@ -533,7 +539,10 @@ class SomEngine:
             self.W, self.W2 = self.W2, self.W
             return
         nb, ne = (0, self.K) if all_nodes else (self.node_begin, self.node_end)
-        _lib.call("somb_hood_update", _ptr(self.S), _ptr(self.cnt), self.d, C.byref(self.cmap),
+        S = self.S
+        if self.cols:   # column blocks -> [K, d] (the all-nodes update of the functional API)
+            S = S.permute(1, 0, 2).reshape(self.K, -1)[:, : self.d].contiguous()
+        _lib.call("somb_hood_update", _ptr(S), _ptr(self.cnt), self.d, C.byref(self.cmap),
                   C.byref(hood), C.c_double(scale), _ptr(self.dist_tab), _ptr(self.W), nb, ne,
                   _ptr(self.W2), _ptr(num_out), _ptr(den_out), _ptr(self.ws), _stream(self.dev))
         if self.sharded and not all_nodes:

@@ -73,30 +73,18 @@ def column_blocks(d: int, p: int) -> list[tuple[int, int]]:
     return [(min(d, r * dc), min(d, (r + 1) * dc)) for r in range(p)]
 
 
-def reduce_scatter_columns(S, dc: int, staging, out, group=None) -> None:
-    """out [K, dc] <- sum over ranks of this rank's column block of S [K, d]
-    (zero-padded to p*dc columns): S is restaged block-major into `staging`
-    [p, K, dc] (one strided copy of the whole blocks, one of the ragged last
-    block; only padding columns are zeroed) so the blocks are contiguous,
-    then reduce-scattered (NCCL; the gloo backend, used by the CPU tests,
-    has no reduce-scatter: all-reduce and take the block)."""
+def reduce_scatter_blocks(S_blocks, out, group=None) -> None:
+    """out [K, dc] <- sum over ranks of block `rank` of S_blocks [p, K, dc]
+    (the column-block-major node sums written by somb_node_sums_*_cols: the
+    blocks are already contiguous, so NCCL reduce-scatters S in place; the
+    gloo backend has no reduce-scatter: all-reduce, then take the block)."""
     import torch.distributed as dist
-    p = staging.shape[0]
-    K, d = S.shape
-    full = min(p, d // dc)                     # complete column blocks
-    if full:
-        staging[:full].copy_(S[:, : full * dc].view(K, full, dc).permute(1, 0, 2))
-    if full < p:
-        staging[full:].zero_()
-        rem = d - full * dc
-        if rem:
-            staging[full, :, :rem].copy_(S[:, full * dc:])
     rank = dist.get_rank(group)
     if dist.get_backend(group) == "nccl":
-        dist.reduce_scatter_tensor(out, staging, op=dist.ReduceOp.SUM, group=group)
+        dist.reduce_scatter_tensor(out, S_blocks, op=dist.ReduceOp.SUM, group=group)
     else:
-        dist.all_reduce(staging, op=dist.ReduceOp.SUM, group=group)
-        out.copy_(staging[rank])
+        dist.all_reduce(S_blocks, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(S_blocks[rank])
 
 
 def allgather_columns(mine, staging, W, d: int, group=None) -> None:

@@ -88,8 +88,8 @@ class SparseEngine(SomEngine):
         self.has_prev = True
 
     def node_sums(self):
-        _lib.call("somb_node_sums_sparse", _ptr(self.rowptr), _ptr(self.col), _ptr(self.val), self.n,
-                  self.d, _ptr(self.bmu), self.K, _ptr(self.S), _ptr(self.cnt), None, _ptr(self.ws),
+        _lib.call("somb_node_sums_sparse_cols", _ptr(self.rowptr), _ptr(self.col), _ptr(self.val), self.n,
+                  self.d, _ptr(self.bmu), self.K, self.dc, _ptr(self.S), _ptr(self.cnt), None, _ptr(self.ws),
                   _stream(self.dev))
 
     def debug_screen_values(self):

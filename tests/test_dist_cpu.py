@@ -15,7 +15,7 @@ import torch.multiprocessing as mp
 import oracle as O
 from paper_1305_1422_b200.parallel import (allgather_columns, allgather_rows, allreduce_sum,
                                            column_blocks, node_slices, partition,
-                                           reduce_scatter_columns, slice_rows)
+                                           reduce_scatter_blocks, slice_rows)
 from paper_1305_1422_b200.datasets import DenseDataset
 
 
@@ -87,9 +87,12 @@ def _worker_cols(rank, world, port, x, w, nx, ny, radius, scale, mt, out):
         bmu, qe, _, _ = O.search_accumulate(xs, w, nx, ny, radius, 0.0, mt, with_accumulators=False)
         s, c = O.node_sums(xs, bmu, k)
         dc = -(-d // world)
-        staging = torch.empty((world, k, dc), dtype=torch.float64)
+        # S column-block-major [world, k, dc], as somb_node_sums_*_cols writes it
+        sp = np.zeros((k, world * dc))
+        sp[:, :d] = s
+        blocks = torch.from_numpy(np.ascontiguousarray(sp.reshape(k, world, dc).transpose(1, 0, 2)))
         mine = torch.empty((k, dc), dtype=torch.float64)
-        reduce_scatter_columns(torch.from_numpy(s), dc, staging, mine)
+        reduce_scatter_blocks(blocks, mine)
         tail = torch.from_numpy(np.concatenate([c, [qe]]))
         allreduce_sum(tail)
         C, qe_all = tail[:k].numpy(), float(tail[-1])

@@ -573,3 +573,45 @@ def test_overflow_pool_exhaustion_sparse():
     eng.search()
     assert np.array_equal(eng.bmu[:n].cpu().numpy(), want)
     assert ((eng.flags[:n].cpu().numpy() & 0x01010101) == 0).all()
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_node_sums_column_blocks_bit_exact(sparse):
+    """somb_node_sums_{dense,sparse}_cols: the multi-rank exchange's
+    column-block-major S [ceil(d/dc)][K][dc] holds exactly the row-major
+    node sums (bit for bit, padding columns zero), for every block width a
+    1..8-rank job uses, including the segmented (> 2048-row) nodes."""
+    from paper_1305_1422_b200 import _lib
+    from paper_1305_1422_b200.engine import _ptr, _stream
+    rng = np.random.default_rng(31)
+    n, d, k = 6000, 37, 50
+    bmu = rng.integers(0, k, n).astype(np.int32)
+    bmu[: n // 2] = 3                                    # one node with 3000 rows: segmented sums
+    if sparse:
+        sp = O.gen_random_sparse(n, d, 0.2, 9)
+        from paper_1305_1422_b200.sparse import SparseEngine
+        eng = SparseEngine(S.SparseDataset(sp.n_dimensions, sp.row_offsets, sp.col_indices, sp.values),
+                             k, 1, S.MapType.PLANAR)
+    else:
+        eng = S.SomEngine(S.DenseDataset(rng.random((n, d), dtype=np.float32)), k, 1, S.MapType.PLANAR)
+    eng.bmu[:n].copy_(torch.from_numpy(bmu))
+    eng.node_sums()
+    want = eng.S.cpu().numpy().copy()                    # row-major [K, d] (dc = d)
+    for dc in (d, 19, 13, 5, 1):
+        nb = -(-d // dc)
+        out = torch.full((nb * k * dc,), np.nan, dtype=torch.float64, device=eng.dev)
+        cnt = torch.empty(k, dtype=torch.float64, device=eng.dev)
+        if sparse:
+            _lib.call("somb_node_sums_sparse_cols", _ptr(eng.rowptr), _ptr(eng.col), _ptr(eng.val), n, d,
+                      _ptr(eng.bmu), k, dc, _ptr(out), _ptr(cnt), None, _ptr(eng.ws), _stream(eng.dev))
+        else:
+            _lib.call("somb_node_sums_dense_cols", _ptr(eng.X), n, d, _ptr(eng.bmu), k, dc, _ptr(out),
+                      _ptr(cnt), None, _ptr(eng.ws), _stream(eng.dev))
+        blk = out.cpu().numpy().reshape(nb, k, dc)
+        got = blk.transpose(1, 0, 2).reshape(k, nb * dc)
+        assert np.array_equal(got[:, :d].view(np.uint64), want.view(np.uint64)), dc
+        assert (got[:, d:] == 0).all()
+        assert np.array_equal(cnt.cpu().numpy(), eng.cnt.cpu().numpy())
+    with pytest.raises(S.errors.InputError):   # block wider than d
+        _lib.call("somb_node_sums_dense_cols", None, n, d, _ptr(eng.bmu), k, d + 1,
+                  _ptr(out), _ptr(cnt), None, _ptr(eng.ws), _stream(eng.dev))
