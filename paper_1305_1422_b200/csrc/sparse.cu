@@ -11,6 +11,7 @@
 // the same window/cap semantics as the dense screen (cand.cuh), then the exact
 // fp64 re-rank evaluates the reference's sparse formula (x2 - 2 dots) + w2.
 #include "cand.cuh"
+#include "rerank.cuh"
 
 namespace somb {
 
@@ -340,8 +341,11 @@ sp_exact_ls_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ c
                    int kp, int K, const double *__restrict__ w2, const double *__restrict__ x2,
                    int *__restrict__ cand, int *__restrict__ bmu, double *__restrict__ d2min,
                    unsigned *__restrict__ done_ctr) {
+    // values staged as fp64 once per warp (v and v 2^896): the per-lane F2F of
+    // every gathered codebook value was the limiter (XU pipe 74% busy, ncu)
     __shared__ int s_col[SP_WARPS][SP_NNZ_BUF];
-    __shared__ float s_val[SP_WARPS][SP_NNZ_BUF];
+    __shared__ double s_vd[SP_WARPS][SP_NNZ_BUF];
+    __shared__ double s_vs[SP_WARPS][SP_NNZ_BUF];
     const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * SP_WARPS + w, GW = (int64_t)gridDim.x * SP_WARPS;
     const int64_t m = (int64_t)*nlist;
@@ -377,15 +381,22 @@ sp_exact_ls_kernel(const int64_t *__restrict__ rowptr, const int *__restrict__ c
                 __syncwarp();
                 for (int t = lane; t < mm; t += 32) {
                     s_col[w][t] = col[e0 + b0 + t];
-                    s_val[w][t] = val[e0 + b0 + t];
+                    const double v = (double)val[e0 + b0 + t];
+                    s_vd[w][t] = v;
+                    s_vs[w][t] = v * kF64Scale;   // exact: |v| < 2^128
                 }
                 __syncwarp();
+                // two components convert on F2F (XU pipe), two by the exact
+                // integer re-exponenting against v 2^896 (ALU pipes): every
+                // product is the exact v a either way, so the sums are
+                // bit-identical to the all-F2F form
 #pragma unroll 8
                 for (int t = 0; t < mm; ++t) {
-                    const double v = (double)s_val[w][t];
+                    const double v = s_vd[w][t], vs = s_vs[w][t];
                     const float4 a = __ldg(reinterpret_cast<const float4 *>(WT + (int64_t)s_col[w][t] * kp + jl));
                     acc[0] = __fma_rn(v, (double)a.x, acc[0]); acc[1] = __fma_rn(v, (double)a.y, acc[1]);
-                    acc[2] = __fma_rn(v, (double)a.z, acc[2]); acc[3] = __fma_rn(v, (double)a.w, acc[3]);
+                    acc[2] = __fma_rn(vs, f32_as_f64_scaled(a.z), acc[2]);
+                    acc[3] = __fma_rn(vs, f32_as_f64_scaled(a.w), acc[3]);
                 }
             }
             const double xx = x2[row];
